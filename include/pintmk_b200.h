@@ -1,0 +1,247 @@
+/*
+ * pintmk_b200.h -- C-ABI of the B200-native all-at-once space-time MLK solve.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `pintmk` (arXiv 2401.00228): solver.multilevel_solve -> fgmres ->
+ * apply_preconditioner -> {matvec, restrict, forward_solve, interpolate}.
+ * Reference paths below are relative to /root/reference/pkg/src/pintmk/.
+ *
+ * The reference is pure Python over numpy/scipy with one Cython seam
+ * (_chain.pyx: factor_tridiag / march_chain).  Its duck-typed seams are the
+ * methods the entry points below replace; each entry cites the reference
+ * method it stands in for.  Every entry:
+ *   - takes caller-allocated DEVICE buffers (fp64, row-major (slices, m) with
+ *     x fastest, exactly the reference's (n_steps+1, n) layout,
+ *     stepper.py:93-94);
+ *   - is stream-ordered on `stream` (a cudaStream_t; NULL = legacy stream);
+ *   - returns 0 on success, a cudaError_t value (< 1000) on a CUDA failure, or
+ *     one of the PMK_ERR_* codes below on a bad argument.  The Python mirror
+ *     maps PMK_ERR_ARG/PMK_ERR_SHAPE to ValueError (reference convention,
+ *     e.g. stepper.py:28-34, solver.py:114-115) and everything else to
+ *     RuntimeError.
+ * No entry point allocates device memory except pmk_hier_create (a few KB of
+ * Krylov scalars); all vectors belong to the caller.
+ */
+#ifndef PINTMK_B200_H
+#define PINTMK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void *pmk_stream_t; /* cudaStream_t */
+
+enum {
+  PMK_OK = 0,
+  PMK_ERR_ARG = 1001,         /* null pointer / out-of-range scalar */
+  PMK_ERR_SHAPE = 1002,       /* inconsistent sizes */
+  PMK_ERR_UNSUPPORTED = 1003, /* stencil / coarse kind not supported */
+  PMK_ERR_STATE = 1004        /* call order violated (e.g. step before begin) */
+};
+
+/* Coarsest-level direct solver kinds (pmk_coarse.kind). */
+enum { PMK_COARSE_DST = 1, PMK_COARSE_DENSE = 2 };
+
+/*
+ * Spatial operator in "right-product" form: (v @ M)_i = sum_j M[j,i] v_j,
+ * i.e. M^T applied to v, which is what the reference matvec computes
+ * (stepper.py:102, `blocks @ self.diag`).  Five slots in ascending column
+ * order, S (i-nx), W (i-1), C (i), E (i+1), N (i+nx); slots whose neighbour
+ * lies outside the grid are skipped.  Products are accumulated in that order
+ * with separately rounded multiply and add, the order scipy's csc_matvecs
+ * uses for the same product.
+ */
+typedef struct pmk_stencil {
+  int32_t var;        /* 0: constant coefficients c[5]; 1: per-point coef */
+  double c[5];        /* constant coefficients, slots S W C E N */
+  const double *coef; /* device [5][m] per-point coefficients (var = 1) */
+} pmk_stencil;
+
+/*
+ * One level's block lower-bidiagonal system [I; -B, D; ...; -B, D]
+ * (stepper.py:66-105).  diag_t holds D^T and sub_t holds B^T so that
+ * out_k = D^T v_k - B^T v_{k-1}; rows listed in `dropped` add B^T v_{k-1}
+ * back (stepper.py:103-104).
+ */
+typedef struct pmk_level {
+  int32_t dim;     /* 1 or 2 */
+  int32_t nx, ny;  /* ny = 1 in 1-D; m = nx*ny */
+  int32_t n_steps; /* slices = n_steps + 1 */
+  pmk_stencil diag_t;
+  pmk_stencil sub_t;
+  const uint8_t *dropped; /* device [n_steps+1] 0/1 mask, or NULL */
+} pmk_level;
+
+/*
+ * Intergrid pair between a level and the next coarser one.
+ * TimePair (intergrid.py:37-63): group_of = NULL, y_* = NULL.
+ * TimeSpacePair (intergrid.py:79-120): Z injection through group_of and the
+ * Y^T averaging as a CSR over coarse points with ascending fine indices.
+ */
+typedef struct pmk_pair {
+  int32_t nu;              /* time coarsening factor (1 = pure space move) */
+  int32_t n_T;             /* coarse steps; fine rows = nu*n_T + 1 */
+  int32_t m_fine, m_coarse;
+  const int32_t *group_of; /* device [m_fine] coarse index of each fine point */
+  const int32_t *y_ptr;    /* device [m_coarse+1] */
+  const int32_t *y_idx;    /* device [nnz] fine indices, ascending per row */
+  const double *y_val;     /* device [nnz] Y entries (1/|group|) */
+} pmk_pair;
+
+/*
+ * Coarsest-level block forward substitution (stepper.py:114-146):
+ *   out_0 = rhs_0,
+ *   out_k = D^{-1} (rhs_k + [k not dropped] * C out_{k-1}),
+ * with C = B in 1-D (_chain.pyx:64-71) and C = B^T in 2-D (stepper.py:144).
+ * DST: D and C are simultaneously diagonal in the orthonormal sine basis
+ *      (pristine Dirichlet Laplacian levels); delta/beta are their
+ *      eigenvalues per mode (p fastest).  One launch chain: x-transform,
+ *      y-transform, segmented per-mode recurrence, inverse transforms.
+ * DENSE: explicit D^{-1} (m x m, row-major) for agglomerated levels whose
+ *      operator is not Toeplitz (intergrid.py:202-227 odd-grid groups).
+ */
+typedef struct pmk_coarse {
+  int32_t kind;
+  int32_t dim, nx, ny, n_steps;
+  const uint8_t *dropped; /* device [n_steps+1] or NULL (exact chain) */
+  const double *sx;       /* DST: [nx][nx] */
+  const double *sy;       /* DST: [ny][ny] (dim 2) */
+  const double *delta;    /* DST: [m] eigenvalues of D */
+  const double *beta;     /* DST: [m] eigenvalues of C */
+  const double *dinv;     /* DENSE: [m][m] */
+  pmk_stencil coupling;   /* DENSE: C as a stencil in row form */
+  double *work0, *work1;  /* device scratch, (n_steps+1)*m doubles each */
+} pmk_coarse;
+
+/* ---------------------------------------------------------------- per-op */
+
+/* BlockBidiagonalSystem.matvec (stepper.py:96-105). */
+int pmk_stmv(const pmk_level *L, const double *v, double *out,
+             pmk_stream_t stream);
+
+/* TimePair.restrict / TimeSpacePair.restrict (intergrid.py:51-56, 106-112).
+ * scratch: (n_T+1)*m_fine doubles, only used for space pairs (may be NULL
+ * for time pairs). */
+int pmk_restrict(const pmk_pair *P, const double *v, double *vh,
+                 double *scratch, pmk_stream_t stream);
+
+/* TimePair.interpolate / TimeSpacePair.interpolate (intergrid.py:58-63,
+ * 114-120). */
+int pmk_interpolate(const pmk_pair *P, const double *w, double *out,
+                    pmk_stream_t stream);
+
+/* Fused solver.py:336-339: vh = Y^T (A v - mu v).  v is read as
+ * v_raw[i] / *v_scale when v_scale is non-NULL (lazily normalised Krylov
+ * basis vector, solver.py:395/420). */
+int pmk_stmv_shift_restrict(const pmk_level *L, const pmk_pair *P, double mu,
+                            const double *v_raw, const double *v_scale,
+                            double *vh, double *scratch, pmk_stream_t stream);
+
+/* Fused solver.py:349,359,403: x = v - Z vt ; w = A x.  x may be NULL (not
+ * stored).  v read as v_raw / *v_scale when v_scale is non-NULL. */
+int pmk_interp_sub_stmv(const pmk_level *L, const pmk_pair *P,
+                        const double *v_raw, const double *v_scale,
+                        const double *vt, double *x, double *w,
+                        pmk_stream_t stream);
+
+/* BlockBidiagonalSystem.forward_solve on the coarsest level
+ * (stepper.py:114-146, _chain.pyx:37-82, linalg.py:62-68). */
+int pmk_coarsest_solve(const pmk_coarse *C, const double *rhs, double *out,
+                       pmk_stream_t stream);
+
+/* Deterministic reductions (np.dot / np.linalg.norm at solver.py:381,407,
+ * 412).  result is a DEVICE scalar.  Fixed grid, fixed summation order:
+ * bitwise reproducible run to run. */
+int pmk_dot(const double *a, const double *b, int64_t n, double *result,
+            pmk_stream_t stream);
+int pmk_nrm2(const double *a, int64_t n, double *result, pmk_stream_t stream);
+
+/* FineSystem.relative_residual numerator (stepper.py:191-193):
+ * result = || rhs - A u ||_2 (device scalar).  tmp: N doubles. */
+int pmk_residual_nrm2(const pmk_level *L, const double *u, const double *rhs,
+                      double *tmp, double *result, pmk_stream_t stream);
+
+/* ----------------------------------------------------- native FGMRES/MLK */
+
+typedef struct pmk_hier pmk_hier;
+
+/* A level hierarchy (solver.py:84-102): levels 0..n_levels-1, the last one
+ * being the coarsest direct solve.  mu: the shift (solver.py:47). */
+pmk_hier *pmk_hier_create(int32_t n_levels, double mu);
+void pmk_hier_destroy(pmk_hier *H);
+
+/* Level idx < n_levels-1: its system, its pair to idx+1 and the inner
+ * FGMRES budget (solver.py:219-235; ignored for idx 0).  The coarsest level
+ * is described by pmk_hier_set_coarse. */
+int pmk_hier_set_level(pmk_hier *H, int32_t idx, const pmk_level *L,
+                       const pmk_pair *P, int32_t budget);
+int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C);
+
+/* Buffers of an inner level (1 <= idx < n_levels-1), or of the coarsest
+ * (idx = n_levels-1: rhs only).  rhs receives the parent's restriction;
+ * w_slots[budget] hold the unnormalised Krylov vectors; child_out[budget]
+ * (size of level idx+1) receive the child solve of each iteration;
+ * ts_scratch ((n_T+1)*m_fine doubles) is required for space pairs. */
+int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs,
+                         double *const *w_slots, double *const *child_out,
+                         int32_t n_slots, double *ts_scratch);
+
+/* fgmres (solver.py:362-456) driven one iteration at a time.
+ * begin: beta = ||rhs||, basis[0] = rhs / beta (lazily).  step j: one
+ * iteration (preconditioner solver.py:323-359, matvec, MGS, Givens), writing
+ * the unnormalised next basis vector into w_next and the child solve into
+ * child_out.  tol > 0 stops the device-side iteration once rel <= tol
+ * (solver.py:438); tol = 0 is the reference's tol=None.  finish: back substitution
+ * and x = sum_i y_i x_i with x_i = v_i - Z vt_i recomputed (no stored
+ * preconditioned vectors). */
+int pmk_fgmres_begin(pmk_hier *H, int32_t idx, const double *rhs,
+                     int32_t max_iter, double tol, pmk_stream_t stream);
+int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *w_next,
+                    double *child_out, pmk_stream_t stream);
+int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x,
+                      pmk_stream_t stream);
+/* Copies the level's fgmres state to the host (synchronises the stream):
+ * scalars[4] = {beta, rel, n_iter, breakdown}; hist[cap] (residual history),
+ * hraw[(cap+1)*cap] (unrotated Hessenberg, row-major, ld = cap) and y[cap]
+ * may be NULL.  *cap (if non-NULL) receives the capacity. */
+int pmk_fgmres_state(pmk_hier *H, int32_t idx, double *scalars, double *hist,
+                     double *hraw, double *y, int32_t *cap,
+                     pmk_stream_t stream);
+
+/* fgmres(hier, idx, rhs, tol=None, max_iter=budget) for an inner level,
+ * entirely on the device (no host synchronisation): the recursion of
+ * solver.py:347-348. Reads the level's registered rhs buffer. */
+int pmk_fgmres_fixed(pmk_hier *H, int32_t idx, double *x,
+                     pmk_stream_t stream);
+
+/* apply_preconditioner (solver.py:323-359) at level idx < n_levels-1:
+ * out = v - Z A_H^{-1} Y^T (A v - mu v).  Uses the registered buffers of
+ * level idx+1 and child_out as the coarse-correction buffer. */
+int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v,
+                             double *child_out, double *out,
+                             pmk_stream_t stream);
+
+/* ------------------------------------------------------------ accounting */
+
+/* Every kernel launch of the library is counted.  pmk_profile_begin(1)
+ * additionally brackets each launch with a CUDA event pair (on the launch
+ * stream) and records its algorithmic bytes / flops; pmk_profile_end
+ * synchronises the device and writes, per category c < *n_categories,
+ * stats[4c .. 4c+3] = {launches, total ms, algorithmic bytes, flops}. */
+int pmk_profile_begin(int32_t with_events);
+int pmk_profile_end(double *stats, int32_t max_categories,
+                    int32_t *n_categories);
+const char *pmk_profile_category(int32_t idx);
+int64_t pmk_launch_count(void);
+
+/* Library identification (for the loaded-.so checks). */
+const char *pmk_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PINTMK_B200_H */

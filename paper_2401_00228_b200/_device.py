@@ -1,0 +1,186 @@
+"""Device descriptors: stencil extraction, level / coarse-solve tables.
+
+Turns the host-side scipy operators of a level (built exactly like the
+reference's, solver.py:105-110) into the flat tables the kernels read:
+
+* a 5-slot stencil (S, W, C, E, N) per operator, either constant (the
+  pristine Laplacian levels) or per point (agglomerated levels);
+* the coarsest-level forward-substitution tables: orthonormal sine
+  transforms plus per-mode eigenvalues (DST), or an explicit inverse
+  (DENSE) for small non-Toeplitz levels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .spatial import dst_eigenvalues_1d, dst_matrix
+
+# Largest spatial size for which the DENSE coarsest solve is allowed
+# (explicit inverse of m*m doubles: 8192^2 * 8 B = 512 MB).
+DENSE_MAX_M = 8192
+
+
+class StencilTable:
+    """Row-form 5-slot stencil of a sparse matrix X: out_i = sum_s c[s, i] *
+    in[i + off_s], offsets (-nx, -1, 0, +1, +nx).  Raises NotImplementedError
+    when X has entries outside the 5-point pattern of the grid."""
+
+    def __init__(self, matrix: sp.spmatrix, nx: int, ny: int):
+        x = sp.csr_matrix(matrix)
+        m = nx * ny
+        if x.shape != (m, m):
+            raise ValueError(f"operator shape {x.shape} does not match grid {nx}x{ny}")
+        coo = x.tocoo()
+        rows, cols, vals = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data
+        off = cols - rows
+        ry, rx = np.divmod(rows, nx)
+        cy, cx = np.divmod(cols, nx)
+        slot = np.full(rows.shape, -1)
+        slot[(off == 0)] = 2
+        same_row = ry == cy
+        slot[(off == -1) & same_row] = 1
+        slot[(off == 1) & same_row] = 3
+        if ny > 1:
+            same_col = rx == cx
+            slot[(off == -nx) & same_col & (slot < 0)] = 0
+            slot[(off == nx) & same_col & (slot < 0)] = 4
+        if np.any(slot < 0):
+            raise NotImplementedError("operator is not a 5-point stencil on the grid")
+        coef = np.zeros((5, m))
+        coef[slot, rows] = vals
+        present = np.zeros((5, m), dtype=bool)
+        present[slot, rows] = True
+        # geometric existence of each neighbour
+        iy, ix = np.divmod(np.arange(m), nx)
+        exists = np.stack([iy > 0, ix > 0, np.ones(m, bool), ix < nx - 1, iy < ny - 1])
+        if ny == 1:
+            exists[0] = False
+            exists[4] = False
+        self.nx, self.ny, self.m = nx, ny, m
+        self.coef = coef
+        constant = bool(np.all(present == exists))
+        consts = np.zeros(5)
+        if constant:
+            for s in range(5):
+                v = coef[s][exists[s]]
+                if v.size and not np.all(v == v[0]):
+                    constant = False
+                    break
+                consts[s] = v[0] if v.size else 0.0
+        self.constant = constant
+        self.consts = consts
+        self._dev = None
+
+    def desc(self) -> _lib.Stencil:
+        st = _lib.Stencil()
+        if self.constant:
+            st.var = 0
+            for s in range(5):
+                st.c[s] = float(self.consts[s])
+            st.coef = None
+        else:
+            import torch
+
+            if self._dev is None:
+                self._dev = torch.from_numpy(np.ascontiguousarray(self.coef)).cuda()
+            st.var = 1
+            st.coef = self._dev.data_ptr()
+        return st
+
+
+def dropped_mask(n_steps: int, dropped) -> np.ndarray | None:
+    if not dropped:
+        return None
+    mask = np.zeros(n_steps + 1, dtype=np.uint8)
+    mask[list(dropped)] = 1
+    return mask
+
+
+class SpectralInfo:
+    """diag = I - a_dt * A and sub = I + b_dt * A with A = factor * (pristine
+    Dirichlet second-difference operator on an nx x ny grid)."""
+
+    def __init__(self, factor: float, a_dt: float, b_dt: float):
+        self.factor = float(factor)
+        self.a_dt = float(a_dt)
+        self.b_dt = float(b_dt)
+
+
+class CoarseSolver:
+    """Device tables of the block forward substitution of one level
+    (reference stepper.py:114-146)."""
+
+    def __init__(self, diag, sub, n_steps, dropped, dim, nx, ny, spectral: SpectralInfo | None):
+        import torch
+
+        _lib.require_cuda()
+        self.dim, self.nx, self.ny = dim, nx, (ny if dim == 2 else 1)
+        self.m = self.nx * self.ny
+        self.n_steps = n_steps
+        self.N = (n_steps + 1) * self.m
+        mask = dropped_mask(n_steps, dropped)
+        self._mask = None if mask is None else torch.from_numpy(mask).cuda()
+        self._keep = []
+        d = _lib.CoarseDesc()
+        d.dim, d.nx, d.ny, d.n_steps = dim, self.nx, self.ny, n_steps
+        d.dropped = None if self._mask is None else self._mask.data_ptr()
+        if spectral is not None:
+            d.kind = _lib.PMK_COARSE_DST
+            ex = dst_eigenvalues_1d(self.nx)
+            if self.ny > 1:
+                ey = dst_eigenvalues_1d(self.ny)
+                lam = spectral.factor * (ey[:, None] + ex[None, :])
+            else:
+                lam = spectral.factor * ex[None, :]
+            lam = lam.ravel()
+            delta = 1.0 - spectral.a_dt * lam
+            beta = 1.0 + spectral.b_dt * lam
+            sx = torch.from_numpy(dst_matrix(self.nx)).cuda()
+            tabs = [sx, torch.from_numpy(delta).cuda(), torch.from_numpy(beta).cuda()]
+            d.sx = sx.data_ptr()
+            if self.ny > 1:
+                sy = torch.from_numpy(dst_matrix(self.ny)).cuda()
+                tabs.append(sy)
+                d.sy = sy.data_ptr()
+            d.delta = tabs[1].data_ptr()
+            d.beta = tabs[2].data_ptr()
+            self._keep += tabs
+            self.work0 = torch.empty(self.N, dtype=torch.float64, device="cuda")
+            self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda") \
+                if self.ny > 1 else None
+            self.kind = "dst"
+        else:
+            if self.m > DENSE_MAX_M:
+                raise NotImplementedError(
+                    f"coarsest level with {self.m} non-Toeplitz unknowns per slice exceeds the "
+                    f"dense-inverse limit ({DENSE_MAX_M}); coarsen further")
+            d.kind = _lib.PMK_COARSE_DENSE
+            dd = np.asarray(sp.csr_matrix(diag).toarray())
+            try:
+                dinv = np.linalg.inv(dd)
+            except np.linalg.LinAlgError as exc:
+                raise np.linalg.LinAlgError(f"factorization failed: {exc}") from exc
+            dinv_t = torch.from_numpy(np.ascontiguousarray(dinv)).cuda()
+            # coupling: B in 1-D (chain march, _chain.pyx:64-71), B^T in 2-D
+            # (stepper.py:144, `out[k-1] @ sub`)
+            cmat = sub if dim == 1 else sp.csr_matrix(sub).T
+            self._coupling = StencilTable(cmat, self.nx, self.ny)
+            d.dinv = dinv_t.data_ptr()
+            d.coupling = self._coupling.desc()
+            self._keep.append(dinv_t)
+            self.work0 = torch.empty(self.m, dtype=torch.float64, device="cuda")
+            self.work1 = None
+            self.kind = "dense"
+        d.work0 = self.work0.data_ptr()
+        d.work1 = None if self.work1 is None else self.work1.data_ptr()
+        self.desc = d
+
+    def solve_into(self, rhs, out) -> None:
+        lib = _lib.load()
+        _lib.check(lib.pmk_coarsest_solve(ctypes.byref(self.desc), _lib.ptr(rhs), _lib.ptr(out),
+                                          _lib.stream_ptr()), "coarsest solve")

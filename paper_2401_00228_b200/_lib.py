@@ -1,0 +1,149 @@
+"""ctypes binding of the C-ABI in include/pintmk_b200.h.
+
+The shared library ``libpmk_b200.so`` (hand-written sm_100a kernels plus the
+native FGMRES recursion) is built in-tree by ``build()`` (nvcc through the
+Makefile in ``csrc/``).  There is no fallback: if the library is missing or
+no CUDA device is present, every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from ctypes import POINTER, c_double, c_int32, c_int64, c_void_p
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpmk_b200.so")
+CSRC = os.path.join(_HERE, "csrc")
+
+PMK_ERR_ARG = 1001
+PMK_ERR_SHAPE = 1002
+PMK_ERR_UNSUPPORTED = 1003
+PMK_ERR_STATE = 1004
+PMK_COARSE_DST = 1
+PMK_COARSE_DENSE = 2
+
+
+class Stencil(ctypes.Structure):
+    _fields_ = [("var", c_int32), ("c", c_double * 5), ("coef", c_void_p)]
+
+
+class LevelDesc(ctypes.Structure):
+    _fields_ = [("dim", c_int32), ("nx", c_int32), ("ny", c_int32),
+                ("n_steps", c_int32), ("diag_t", Stencil), ("sub_t", Stencil),
+                ("dropped", c_void_p)]
+
+
+class PairDesc(ctypes.Structure):
+    _fields_ = [("nu", c_int32), ("n_T", c_int32), ("m_fine", c_int32),
+                ("m_coarse", c_int32), ("group_of", c_void_p), ("y_ptr", c_void_p),
+                ("y_idx", c_void_p), ("y_val", c_void_p)]
+
+
+class CoarseDesc(ctypes.Structure):
+    _fields_ = [("kind", c_int32), ("dim", c_int32), ("nx", c_int32), ("ny", c_int32),
+                ("n_steps", c_int32), ("dropped", c_void_p), ("sx", c_void_p),
+                ("sy", c_void_p), ("delta", c_void_p), ("beta", c_void_p),
+                ("dinv", c_void_p), ("coupling", Stencil), ("work0", c_void_p),
+                ("work1", c_void_p)]
+
+
+# name -> (restype, argtypes); exactly the functions include/pintmk_b200.h declares
+SIGNATURES = {
+    "pmk_version": (ctypes.c_char_p, []),
+    "pmk_stmv": (c_int32, [POINTER(LevelDesc), c_void_p, c_void_p, c_void_p]),
+    "pmk_restrict": (c_int32, [POINTER(PairDesc), c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmk_interpolate": (c_int32, [POINTER(PairDesc), c_void_p, c_void_p, c_void_p]),
+    "pmk_stmv_shift_restrict": (c_int32, [POINTER(LevelDesc), POINTER(PairDesc), c_double,
+                                          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmk_interp_sub_stmv": (c_int32, [POINTER(LevelDesc), POINTER(PairDesc), c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "pmk_coarsest_solve": (c_int32, [POINTER(CoarseDesc), c_void_p, c_void_p, c_void_p]),
+    "pmk_dot": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "pmk_nrm2": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "pmk_residual_nrm2": (c_int32, [POINTER(LevelDesc), c_void_p, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
+    "pmk_hier_create": (c_void_p, [c_int32, c_double]),
+    "pmk_hier_destroy": (None, [c_void_p]),
+    "pmk_hier_set_level": (c_int32, [c_void_p, c_int32, POINTER(LevelDesc),
+                                     POINTER(PairDesc), c_int32]),
+    "pmk_hier_set_coarse": (c_int32, [c_void_p, POINTER(CoarseDesc)]),
+    "pmk_hier_set_buffers": (c_int32, [c_void_p, c_int32, c_void_p, POINTER(c_void_p),
+                                       POINTER(c_void_p), c_int32, c_void_p]),
+    "pmk_fgmres_begin": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_double, c_void_p]),
+    "pmk_fgmres_step": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    "pmk_fgmres_finish": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
+    "pmk_fgmres_state": (c_int32, [c_void_p, c_int32, POINTER(c_double), POINTER(c_double),
+                                   POINTER(c_double), POINTER(c_double), POINTER(c_int32),
+                                   c_void_p]),
+    "pmk_fgmres_fixed": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
+    "pmk_apply_preconditioner": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
+                                           c_void_p]),
+}
+
+_lib = None
+
+
+def build(force: bool = False, quiet: bool = True) -> str:
+    """Compile libpmk_b200.so for sm_100a in-tree (nvcc via csrc/Makefile)."""
+    if force:
+        subprocess.run(["make", "-C", CSRC, "clean"], check=True,
+                       capture_output=quiet)
+    proc = subprocess.run(["make", "-C", CSRC, "-j4"], capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(f"building libpmk_b200.so failed:\n{proc.stdout}\n{proc.stderr}")
+    return LIB_PATH
+
+
+def load():
+    """Load the shared library (building it first if absent); raise if impossible."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        build()
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class PmkError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str) -> None:
+    if rc == 0:
+        return
+    if rc in (PMK_ERR_ARG, PMK_ERR_SHAPE):
+        raise ValueError(f"{what}: invalid argument (code {rc})")
+    if rc == PMK_ERR_UNSUPPORTED:
+        raise NotImplementedError(f"{what}: unsupported configuration")
+    if rc == PMK_ERR_STATE:
+        raise PmkError(f"{what}: call order violated")
+    raise PmkError(f"{what}: CUDA error {rc}")
+
+
+def require_cuda():
+    """The product path has no CPU fallback: fail loudly without a GPU."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2401_00228_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    load()
+    return torch
+
+
+def stream_ptr():
+    import torch
+
+    return c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t) -> c_void_p:
+    return c_void_p(0 if t is None else t.data_ptr())

@@ -1,0 +1,630 @@
+// pmk_api.cu -- extern "C" entry points (include/pintmk_b200.h) and the
+// native FGMRES / MLK recursion.
+//
+// The recursion mirrors reference solver.py:323-456 step for step:
+//
+//   fgmres(level, rhs, tol, max_iter)          solver.py:362-456
+//     beta = ||rhs||; v_0 = rhs / beta         (begin_kernel; v_0 kept lazy)
+//     for j:
+//       x_j = apply_preconditioner(v_j)        solver.py:323-359
+//          vh = Y^T (A v_j - mu v_j)           K-MVR (one pass)
+//          vt = coarsest forward_solve(vh)     or fgmres(level+1, vh, None, budget)
+//          x_j = v_j - Z vt                    fused into K-IMV below
+//       w = A x_j                              K-IMV (+ partial <w, v_0>)
+//       MGS                                    j+1 fused passes
+//       h[j+1,j], breakdown, Givens, rel       finish_col_kernel (device)
+//     y = R^{-1} g ; x = sum y_i x_i           backsolve + assemble (x_i recomputed)
+//
+// Nothing in an inner solve synchronises with the host: the breakdown /
+// beta == 0 exits of the reference are device flags that turn the remaining
+// launches of that invocation into no-ops.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <vector>
+
+#include "pmk_internal.cuh"
+#include "pmk_krylov.cuh"
+
+using namespace pmk;
+
+// ------------------------------------------------------------- accounting
+namespace {
+struct ProfRec {
+  int cat;
+  double bytes, flops;
+  cudaEvent_t a, b;
+};
+std::atomic<int64_t> g_launches{0};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<ProfRec> g_recs;
+std::vector<cudaEvent_t> g_pool;
+size_t g_pool_used = 0;
+const char *kCatNames[prof::kNumCat] = {"march_mv", "march_mvr", "march_imv", "mgs_pass",
+                                         "reduce",   "fgmres_small", "assemble", "coarse_gemm",
+                                         "coarse_recurrence", "coarse_misc", "transfer"};
+
+cudaEvent_t pool_event() {
+  if (g_pool_used == g_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    g_pool.push_back(e);
+  }
+  return g_pool[g_pool_used++];
+}
+}  // namespace
+
+namespace pmk {
+namespace prof {
+Scope::Scope(int cat, double bytes, double flops, cudaStream_t s) : rec(-1), stream(s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!g_prof_on) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  ProfRec r{cat, bytes, flops, pool_event(), pool_event()};
+  if (!r.a || !r.b) return;
+  cudaEventRecord(r.a, s);
+  rec = (int)g_recs.size();
+  g_recs.push_back(r);
+}
+Scope::~Scope() {
+  if (rec < 0) return;
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  cudaEventRecord(g_recs[rec].b, stream);
+}
+}  // namespace prof
+}  // namespace pmk
+
+namespace {
+
+struct LevelRT {
+  bool set = false;
+  pmk_level L{};
+  pmk_pair P{};
+  int budget = 0;
+  int64_t N = 0;
+  // registered buffers (inner levels / coarsest rhs)
+  double *rhs = nullptr;
+  std::vector<double *> w_slots, child_out;
+  double *ts_scratch = nullptr;
+  // device state
+  KState *d_state = nullptr;  // header in device memory
+  KState h_state{};           // host copy of the pointers
+  void *d_block = nullptr;
+  int cap = 0;
+  double *partA = nullptr, *partB = nullptr;
+  double tol = 0.0;
+  // current invocation
+  std::vector<const double *> vraw;  // raw basis vectors, index l
+  std::vector<const double *> vt;    // child outputs, iteration j
+  const int *parent_live = nullptr;
+};
+
+}  // namespace
+
+struct pmk_hier {
+  int n_levels = 0;
+  double mu = 1.0;
+  std::vector<LevelRT> lv;
+  pmk_coarse coarse{};
+  bool has_coarse = false;
+  double *coarse_rhs = nullptr;
+};
+
+namespace {
+
+inline cudaStream_t cs(pmk_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t level_N(const pmk_level &L) {
+  const int64_t m = (int64_t)L.nx * (L.dim == 2 ? L.ny : 1);
+  return (int64_t)(L.n_steps + 1) * m;
+}
+
+int check_level(const pmk_level *L) {
+  PMK_RETURN_IF(!L, PMK_ERR_ARG);
+  PMK_RETURN_IF(L->dim != 1 && L->dim != 2, PMK_ERR_ARG);
+  PMK_RETURN_IF(L->nx < 1 || L->ny < 1 || L->n_steps < 0, PMK_ERR_SHAPE);
+  PMK_RETURN_IF(L->dim == 1 && L->ny != 1, PMK_ERR_SHAPE);
+  PMK_RETURN_IF(L->diag_t.var && !L->diag_t.coef, PMK_ERR_ARG);
+  PMK_RETURN_IF(L->sub_t.var && !L->sub_t.coef, PMK_ERR_ARG);
+  return 0;
+}
+
+int check_pair(const pmk_level &L, const pmk_pair *P) {
+  PMK_RETURN_IF(!P, PMK_ERR_ARG);
+  PMK_RETURN_IF(P->nu < 1 || P->n_T < 0, PMK_ERR_ARG);
+  PMK_RETURN_IF(P->nu * P->n_T != L.n_steps, PMK_ERR_SHAPE);
+  PMK_RETURN_IF(P->m_fine != L.nx * L.ny, PMK_ERR_SHAPE);
+  const bool space = P->group_of != nullptr;
+  PMK_RETURN_IF(space && (!P->y_ptr || !P->y_idx || !P->y_val), PMK_ERR_ARG);
+  PMK_RETURN_IF(!space && P->m_coarse != P->m_fine, PMK_ERR_SHAPE);
+  return 0;
+}
+
+MarchParams base_params(const pmk_level &L) {
+  MarchParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.nx = L.nx;
+  p.ny = (L.dim == 2) ? L.ny : 1;
+  p.m = p.nx * p.ny;
+  p.n_steps = L.n_steps;
+  p.P = L.diag_t;
+  p.Q = L.sub_t;
+  p.dropped = L.dropped;
+  p.nu = 1;
+  p.m_coarse = p.m;
+  return p;
+}
+
+// vh = Y^T (A v - mu v)
+int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
+           const double *v_scale, double *vh, double *scratch, const int *live, cudaStream_t s) {
+  MarchParams p = base_params(L);
+  p.v = v;
+  p.v_scale = v_scale;
+  p.mu = mu;
+  p.nu = P.nu;
+  const bool space = P.group_of != nullptr;
+  PMK_RETURN_IF(space && !scratch, PMK_ERR_ARG);
+  p.vh = space ? scratch : vh;
+  p.live = live;
+  int rc = launch_march(kModeMVR, p, s, nullptr);
+  if (rc) return rc;
+  if (space) return launch_ts_gather(P, scratch, vh, live, s);
+  return 0;
+}
+
+// x = v - Z vt ; w = A x ; partial <w, v0>
+int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double *v_scale,
+           const double *vt, double *x, double *w, const double *v0, const double *v0_scale,
+           double *partials, int *n_partials, const int *live, cudaStream_t s) {
+  MarchParams p = base_params(L);
+  p.v = v;
+  p.v_scale = v_scale;
+  p.nu = P.nu;
+  p.vt = vt;
+  p.group_of = P.group_of;
+  p.m_coarse = P.m_coarse;
+  p.x_out = x;
+  p.out = w;
+  p.v0 = v0;
+  p.v0_scale = v0_scale;
+  p.partials = partials;
+  p.live = live;
+  return launch_march(kModeIMV, p, s, n_partials);
+}
+
+int alloc_state(LevelRT &R, int cap) {
+  if (R.cap >= cap && R.d_state) return 0;
+  if (R.d_block) {
+    cudaFree(R.d_block);
+    R.d_block = nullptr;
+  }
+  const size_t nh = (size_t)(cap + 1) * cap;
+  const size_t n_doubles = 2 * nh + 7 * (size_t)(cap + 1) + 2 * kMaxPartials;
+  const size_t bytes = sizeof(KState) + 64 + n_doubles * sizeof(double);
+  PMK_CUDA_TRY(cudaMalloc(&R.d_block, bytes));
+  PMK_CUDA_TRY(cudaMemset(R.d_block, 0, bytes));
+  char *base = static_cast<char *>(R.d_block);
+  R.d_state = reinterpret_cast<KState *>(base);
+  double *d = reinterpret_cast<double *>(base + ((sizeof(KState) + 63) / 64) * 64);
+  KState h{};
+  h.h = d;
+  d += nh;
+  h.hraw = d;
+  d += nh;
+  h.cs = d;
+  d += cap + 1;
+  h.sn = d;
+  d += cap + 1;
+  h.g = d;
+  d += cap + 1;
+  h.y = d;
+  d += cap + 1;
+  h.vscale = d;
+  d += cap + 1;
+  h.hist = d;
+  d += cap + 1;
+  d += cap + 1;  // spare
+  R.partA = d;
+  d += kMaxPartials;
+  R.partB = d;
+  R.h_state = h;
+  R.cap = cap;
+  PMK_CUDA_TRY(cudaMemcpy(R.d_state, &h, sizeof(KState), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+inline const int *live_ptr(const LevelRT &R) { return &R.d_state->live; }
+
+int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double tol,
+                 const int *parent_live, cudaStream_t s) {
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
+  PMK_RETURN_IF(!rhs || max_iter < 1, PMK_ERR_ARG);
+  int rc = alloc_state(R, max_iter);
+  if (rc) return rc;
+  R.tol = tol;
+  R.parent_live = parent_live;
+  rc = launch_dot_partials(rhs, nullptr, rhs, nullptr, R.N, R.partA, parent_live, s);
+  if (rc) return rc;
+  rc = launch_begin(R.d_state, R.partA, kRedBlocks, parent_live, s);
+  if (rc) return rc;
+  R.vraw.assign(1, rhs);
+  R.vt.clear();
+  return 0;
+}
+
+int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s);
+
+// Child solve of level idx: vt = A_{idx+1}^{-1} vh (approximately).
+int child_solve(pmk_hier *H, int idx, double *out, const int *live, cudaStream_t s) {
+  const int child = idx + 1;
+  if (child == H->n_levels - 1) {
+    PMK_RETURN_IF(!H->has_coarse || !H->coarse_rhs, PMK_ERR_STATE);
+    return coarse_solve(H->coarse, H->coarse_rhs, out, live, s);
+  }
+  return fgmres_fixed(H, child, out, live, s);
+}
+
+double *child_rhs(pmk_hier *H, int idx) {
+  const int child = idx + 1;
+  if (child == H->n_levels - 1) return H->coarse_rhs;
+  return H->lv[child].rhs;
+}
+
+int fgmres_step(pmk_hier *H, int idx, int j, double *w_next, double *child_out, cudaStream_t s) {
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
+  PMK_RETURN_IF(j != (int)R.vt.size() || j >= R.cap, PMK_ERR_STATE);
+  PMK_RETURN_IF(!w_next || !child_out, PMK_ERR_ARG);
+  double *vh = child_rhs(H, idx);
+  PMK_RETURN_IF(!vh, PMK_ERR_STATE);
+  const int *live = live_ptr(R);
+  const KState &K = R.h_state;
+  const double *vj = R.vraw[j];
+  const double *sj = K.vscale + j;
+  // apply_preconditioner (solver.py:336-359)
+  int rc = do_mvr(R.L, R.P, H->mu, vj, sj, vh, R.ts_scratch, live, s);
+  if (rc) return rc;
+  rc = child_solve(H, idx, child_out, live, s);
+  if (rc) return rc;
+  // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407)
+  int np = 0;
+  rc = do_imv(R.L, R.P, vj, sj, child_out, nullptr, w_next, R.vraw[0], K.vscale, R.partA, &np,
+              live, s);
+  if (rc) return rc;
+  // MGS (solver.py:405-408), then ||w|| on the last pass (solver.py:412)
+  double *prev = R.partA, *cur = R.partB;
+  int n_prev = np;
+  for (int l = 0; l <= j; ++l) {
+    const double *vn = (l < j) ? R.vraw[l + 1] : nullptr;
+    rc = launch_mgs_pass(R.d_state, R.cap, l, j, w_next, R.vraw[l], K.vscale + l, vn,
+                         K.vscale + l + 1, R.N, prev, n_prev, cur, s);
+    if (rc) return rc;
+    double *t = prev;
+    prev = cur;
+    cur = t;
+    n_prev = kRedBlocks;
+  }
+  rc = launch_finish_col(R.d_state, R.cap, j, prev, n_prev, R.tol, s);
+  if (rc) return rc;
+  R.vraw.push_back(w_next);
+  R.vt.push_back(child_out);
+  return 0;
+}
+
+int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
+  PMK_RETURN_IF(!x, PMK_ERR_ARG);
+  int rc = launch_backsolve(R.d_state, R.cap, s);
+  if (rc) return rc;
+  const int n = (int)R.vt.size();
+  const int m = R.P.m_fine;
+  int first = 0;
+  do {
+    AssembleArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.count = 0;
+    for (int l = first; l < n && a.count < kAsmChunk; ++l) {
+      a.vraw[a.count] = R.vraw[l];
+      a.vt[a.count] = R.vt[l];
+      ++a.count;
+    }
+    rc = launch_assemble(R.d_state, a, x, R.N, m, R.P.nu, R.P.m_coarse, R.P.group_of, first, s);
+    if (rc) return rc;
+    first += kAsmChunk;
+  } while (first < n);
+  return 0;
+}
+
+int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s) {
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set || !R.rhs, PMK_ERR_STATE);
+  PMK_RETURN_IF((int)R.w_slots.size() < R.budget || (int)R.child_out.size() < R.budget,
+                PMK_ERR_STATE);
+  int rc = fgmres_begin(H, idx, R.rhs, R.budget, 0.0, parent_live, s);
+  if (rc) return rc;
+  for (int j = 0; j < R.budget; ++j) {
+    rc = fgmres_step(H, idx, j, R.w_slots[j], R.child_out[j], s);
+    if (rc) return rc;
+  }
+  return fgmres_finish(H, idx, x, s);
+}
+
+// Internal scratch for the stand-alone reductions.
+std::mutex g_scratch_mu;
+double *g_scratch = nullptr;
+double *scratch_partials() {
+  std::lock_guard<std::mutex> g(g_scratch_mu);
+  if (!g_scratch) {
+    if (cudaMalloc(&g_scratch, kMaxPartials * sizeof(double)) != cudaSuccess) g_scratch = nullptr;
+  }
+  return g_scratch;
+}
+
+}  // namespace
+
+// ============================================================== C-ABI
+extern "C" {
+
+const char *pmk_version(void) { return "pintmk_b200 0.1 sm_100a"; }
+
+int64_t pmk_launch_count(void) { return g_launches.load(); }
+
+int pmk_profile_begin(int32_t with_events) {
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_recs.clear();
+  g_pool_used = 0;
+  g_prof_on = with_events != 0;
+  return 0;
+}
+
+int pmk_profile_end(double *stats, int32_t max_categories, int32_t *n_categories) {
+  PMK_CUDA_TRY(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = false;
+  const int nc = prof::kNumCat < max_categories ? prof::kNumCat : max_categories;
+  if (stats)
+    for (int i = 0; i < 4 * nc; ++i) stats[i] = 0.0;
+  for (const ProfRec &r : g_recs) {
+    if (r.cat >= nc || !stats) continue;
+    float ms = 0.f;
+    PMK_CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    stats[4 * r.cat + 0] += 1.0;
+    stats[4 * r.cat + 1] += ms;
+    stats[4 * r.cat + 2] += r.bytes;
+    stats[4 * r.cat + 3] += r.flops;
+  }
+  g_recs.clear();
+  g_pool_used = 0;
+  if (n_categories) *n_categories = nc;
+  return 0;
+}
+
+const char *pmk_profile_category(int32_t idx) {
+  return (idx >= 0 && idx < prof::kNumCat) ? kCatNames[idx] : "";
+}
+
+int pmk_stmv(const pmk_level *L, const double *v, double *out, pmk_stream_t stream) {
+  int rc = check_level(L);
+  if (rc) return rc;
+  PMK_RETURN_IF(!v || !out, PMK_ERR_ARG);
+  MarchParams p = base_params(*L);
+  p.v = v;
+  p.out = out;
+  return launch_march(kModeMV, p, cs(stream), nullptr);
+}
+
+int pmk_restrict(const pmk_pair *P, const double *v, double *vh, double *scratch,
+                 pmk_stream_t stream) {
+  PMK_RETURN_IF(!P || !v || !vh, PMK_ERR_ARG);
+  if (P->group_of) {
+    PMK_RETURN_IF(!scratch, PMK_ERR_ARG);
+    pmk_pair tp = *P;
+    int rc = launch_restrict_time(tp, v, scratch, cs(stream));
+    if (rc) return rc;
+    return launch_ts_gather(*P, scratch, vh, nullptr, cs(stream));
+  }
+  return launch_restrict_time(*P, v, vh, cs(stream));
+}
+
+int pmk_interpolate(const pmk_pair *P, const double *w, double *out, pmk_stream_t stream) {
+  PMK_RETURN_IF(!P || !w || !out, PMK_ERR_ARG);
+  return launch_interpolate(*P, w, out, cs(stream));
+}
+
+int pmk_stmv_shift_restrict(const pmk_level *L, const pmk_pair *P, double mu,
+                            const double *v_raw, const double *v_scale, double *vh,
+                            double *scratch, pmk_stream_t stream) {
+  int rc = check_level(L);
+  if (rc) return rc;
+  rc = check_pair(*L, P);
+  if (rc) return rc;
+  PMK_RETURN_IF(!v_raw || !vh, PMK_ERR_ARG);
+  return do_mvr(*L, *P, mu, v_raw, v_scale, vh, scratch, nullptr, cs(stream));
+}
+
+int pmk_interp_sub_stmv(const pmk_level *L, const pmk_pair *P, const double *v_raw,
+                        const double *v_scale, const double *vt, double *x, double *w,
+                        pmk_stream_t stream) {
+  int rc = check_level(L);
+  if (rc) return rc;
+  rc = check_pair(*L, P);
+  if (rc) return rc;
+  PMK_RETURN_IF(!v_raw || !vt || !w, PMK_ERR_ARG);
+  return do_imv(*L, *P, v_raw, v_scale, vt, x, w, v_raw, v_scale, nullptr, nullptr, nullptr,
+                cs(stream));
+}
+
+int pmk_coarsest_solve(const pmk_coarse *C, const double *rhs, double *out,
+                       pmk_stream_t stream) {
+  PMK_RETURN_IF(!C || !rhs || !out, PMK_ERR_ARG);
+  return coarse_solve(*C, rhs, out, nullptr, cs(stream));
+}
+
+int pmk_dot(const double *a, const double *b, int64_t n, double *result, pmk_stream_t stream) {
+  PMK_RETURN_IF(!a || !b || !result || n < 0, PMK_ERR_ARG);
+  double *part = scratch_partials();
+  PMK_RETURN_IF(!part, (int)cudaErrorMemoryAllocation);
+  int rc = launch_dot_partials(a, nullptr, b, nullptr, n, part, nullptr, cs(stream));
+  if (rc) return rc;
+  return launch_reduce_to_scalar(part, kRedBlocks, result, 0, cs(stream));
+}
+
+int pmk_nrm2(const double *a, int64_t n, double *result, pmk_stream_t stream) {
+  PMK_RETURN_IF(!a || !result || n < 0, PMK_ERR_ARG);
+  double *part = scratch_partials();
+  PMK_RETURN_IF(!part, (int)cudaErrorMemoryAllocation);
+  int rc = launch_dot_partials(a, nullptr, a, nullptr, n, part, nullptr, cs(stream));
+  if (rc) return rc;
+  return launch_reduce_to_scalar(part, kRedBlocks, result, 1, cs(stream));
+}
+
+int pmk_residual_nrm2(const pmk_level *L, const double *u, const double *rhs, double *tmp,
+                      double *result, pmk_stream_t stream) {
+  int rc = check_level(L);
+  if (rc) return rc;
+  PMK_RETURN_IF(!u || !rhs || !tmp || !result, PMK_ERR_ARG);
+  rc = pmk_stmv(L, u, tmp, stream);
+  if (rc) return rc;
+  double *part = scratch_partials();
+  PMK_RETURN_IF(!part, (int)cudaErrorMemoryAllocation);
+  rc = launch_diffsq_partials(rhs, tmp, level_N(*L), part, cs(stream));
+  if (rc) return rc;
+  return launch_reduce_to_scalar(part, kRedBlocks, result, 1, cs(stream));
+}
+
+pmk_hier *pmk_hier_create(int32_t n_levels, double mu) {
+  if (n_levels < 2 || mu == 0.0) return nullptr;
+  pmk_hier *H = new (std::nothrow) pmk_hier();
+  if (!H) return nullptr;
+  H->n_levels = n_levels;
+  H->mu = mu;
+  H->lv.resize(n_levels - 1);
+  return H;
+}
+
+void pmk_hier_destroy(pmk_hier *H) {
+  if (!H) return;
+  for (auto &R : H->lv)
+    if (R.d_block) cudaFree(R.d_block);
+  delete H;
+}
+
+int pmk_hier_set_level(pmk_hier *H, int32_t idx, const pmk_level *L, const pmk_pair *P,
+                       int32_t budget) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
+  int rc = check_level(L);
+  if (rc) return rc;
+  rc = check_pair(*L, P);
+  if (rc) return rc;
+  PMK_RETURN_IF(idx > 0 && budget < 1, PMK_ERR_ARG);
+  LevelRT &R = H->lv[idx];
+  R.L = *L;
+  R.P = *P;
+  R.budget = budget;
+  R.N = level_N(*L);
+  R.set = true;
+  if (idx > 0) return alloc_state(R, budget);
+  return 0;
+}
+
+int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C) {
+  PMK_RETURN_IF(!H || !C, PMK_ERR_ARG);
+  PMK_RETURN_IF(C->kind != PMK_COARSE_DST && C->kind != PMK_COARSE_DENSE, PMK_ERR_UNSUPPORTED);
+  H->coarse = *C;
+  H->has_coarse = true;
+  return 0;
+}
+
+int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *w_slots,
+                         double *const *child_out, int32_t n_slots, double *ts_scratch) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels || !rhs, PMK_ERR_ARG);
+  if (idx == H->n_levels - 1) {
+    H->coarse_rhs = rhs;
+    return 0;
+  }
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
+  PMK_RETURN_IF(n_slots < 0 || (n_slots > 0 && (!w_slots || !child_out)), PMK_ERR_ARG);
+  PMK_RETURN_IF(R.P.group_of && !ts_scratch, PMK_ERR_ARG);
+  R.rhs = rhs;
+  R.w_slots.assign(w_slots, w_slots + n_slots);
+  R.child_out.assign(child_out, child_out + n_slots);
+  R.ts_scratch = ts_scratch;
+  return 0;
+}
+
+int pmk_fgmres_begin(pmk_hier *H, int32_t idx, const double *rhs, int32_t max_iter, double tol,
+                     pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
+  return fgmres_begin(H, idx, rhs, max_iter, tol, nullptr, cs(stream));
+}
+
+int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *w_next, double *child_out,
+                    pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
+  return fgmres_step(H, idx, j, w_next, child_out, cs(stream));
+}
+
+int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x, pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
+  return fgmres_finish(H, idx, x, cs(stream));
+}
+
+int pmk_fgmres_state(pmk_hier *H, int32_t idx, double *scalars, double *hist, double *hraw,
+                     double *y, int32_t *cap, pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.d_state, PMK_ERR_STATE);
+  cudaStream_t s = cs(stream);
+  KState k;
+  PMK_CUDA_TRY(cudaMemcpyAsync(&k, R.d_state, sizeof(KState), cudaMemcpyDeviceToHost, s));
+  if (hist)
+    PMK_CUDA_TRY(cudaMemcpyAsync(hist, R.h_state.hist, R.cap * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  if (hraw)
+    PMK_CUDA_TRY(cudaMemcpyAsync(hraw, R.h_state.hraw, (size_t)(R.cap + 1) * R.cap * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
+  if (y)
+    PMK_CUDA_TRY(
+        cudaMemcpyAsync(y, R.h_state.y, R.cap * sizeof(double), cudaMemcpyDeviceToHost, s));
+  PMK_CUDA_TRY(cudaStreamSynchronize(s));
+  if (scalars) {
+    scalars[0] = k.beta;
+    scalars[1] = k.rel;
+    scalars[2] = (double)k.n_iter;
+    scalars[3] = (double)k.breakdown;
+  }
+  if (cap) *cap = R.cap;
+  return 0;
+}
+
+int pmk_fgmres_fixed(pmk_hier *H, int32_t idx, double *x, pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 1 || idx >= H->n_levels - 1 || !x, PMK_ERR_ARG);
+  return fgmres_fixed(H, idx, x, nullptr, cs(stream));
+}
+
+int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v, double *child_out,
+                             double *out, pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1 || !v || !child_out || !out, PMK_ERR_ARG);
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
+  cudaStream_t s = cs(stream);
+  double *vh = child_rhs(H, idx);
+  PMK_RETURN_IF(!vh, PMK_ERR_STATE);
+  int rc = do_mvr(R.L, R.P, H->mu, v, nullptr, vh, R.ts_scratch, nullptr, s);
+  if (rc) return rc;
+  rc = child_solve(H, idx, child_out, nullptr, s);
+  if (rc) return rc;
+  // out = v - Z vt (the matvec output of the fused kernel is not needed)
+  return do_imv(R.L, R.P, v, nullptr, child_out, out, nullptr, nullptr, nullptr, nullptr,
+                nullptr, nullptr, s);
+}
+
+}  // extern "C"

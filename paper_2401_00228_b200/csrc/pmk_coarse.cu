@@ -1,0 +1,259 @@
+// pmk_coarse.cu -- coarsest-level block forward substitution (reference
+// stepper.py:114-146, _chain.pyx:37-82, linalg.py:62-68).
+//
+//   out_0 = rhs_0
+//   out_k = D^{-1} (rhs_k + [k not dropped] C out_{k-1})
+//
+// DST path (pristine Dirichlet-Laplacian levels, i.e. every level reached by
+// time moves only): D = I - a dt A and C = I + (1-a) dt A are simultaneously
+// diagonal in the orthonormal sine basis S (S = S^T = S^{-1}).  The solve is
+//   R^ = S_y R S_x            (two fp64 GEMMs over all slices at once)
+//   u^_k = (r^_k + beta u^_{k-1}) / delta   per mode, segmented at dropped k
+//   out = S_y U^ S_x          (two GEMMs)
+// so the exact chain (coarsest_n_cgs = 0) and any chunked decoupling
+// (perturb_decouple, intergrid.py:299-311) cost the same and are parallel
+// over all m modes; the sequential dimension is only the scalar recurrence.
+//
+// DENSE path (agglomerated levels with non-Toeplitz operators): explicit
+// D^{-1}, one stencil + GEMV launch pair per slice.
+//
+// This translation unit keeps FMA contraction on (DFMA GEMM); the result
+// differs from the reference's LU / Thomas solve by rounding only.
+#include "pmk_internal.cuh"
+
+namespace pmk {
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+// C[b] = A[b] * B[b], all row-major; 256 threads, 4x4 outputs per thread
+// (rows ty + 16 i, cols tx + 16 j -> conflict-free shared-memory reads).
+__global__ void __launch_bounds__(256)
+    dgemm_nn_kernel(int M, int N, int K, const double *__restrict__ A, int lda, int64_t sA,
+                    const double *__restrict__ B, int ldb, int64_t sB, double *__restrict__ C,
+                    int ldc, int64_t sC, const int *live) {
+  if (!is_live(live)) return;
+  __shared__ double As[2][BK][BM + 1];
+  __shared__ double Bs[2][BK][BN];
+  const int bz = blockIdx.z;
+  A += bz * sA;
+  B += bz * sB;
+  C += bz * sC;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+
+  double ra[4], rb[4];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = (t >> 4) + 16 * q, c = t & 15;
+      const int gm = m0 + r, gk = k0 + c;
+      ra[q] = (gm < M && gk < K) ? A[(int64_t)gm * lda + gk] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int r = (t >> 6) + 4 * q, c = t & 63;
+      const int gk = k0 + r, gn = n0 + c;
+      rb[q] = (gk < K && gn < N) ? B[(int64_t)gk * ldb + gn] : 0.0;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) As[buf][t & 15][(t >> 4) + 16 * q] = ra[q];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Bs[buf][(t >> 6) + 4 * q][t & 63] = rb[q];
+  };
+
+  const int nk = (K + BK - 1) / BK;
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) gload((kt + 1) * BK);
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) sstore(buf ^ 1);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx + 16 * j;
+      if (gn < N) C[(int64_t)gm * ldc + gn] = acc[i][j];
+    }
+  }
+}
+
+int gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B, int ldb,
+         int64_t sB, double *C, int ldc, int64_t sC, int batch, const int *live, cudaStream_t s) {
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  dgemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+// Segmented per-mode first-order recurrence, in place on X ((n+1) x m).
+// Loads are batched ahead of the dependent chain (the store to X would
+// otherwise serialise them).
+constexpr int kRecBatch = 8;
+__global__ void __launch_bounds__(256)
+    dst_recurrence_kernel(double *X, const double *delta, const double *beta,
+                          const uint8_t *dropped, int n_steps, int m, const int *live) {
+  if (!is_live(live)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const double d = delta[i], b = beta[i];
+  double u = X[i];  // transformed rhs_0 == transformed out_0
+  for (int k0 = 1; k0 <= n_steps; k0 += kRecBatch) {
+    double r[kRecBatch];
+#pragma unroll
+    for (int q = 0; q < kRecBatch; ++q) {
+      const int k = k0 + q;
+      r[q] = (k <= n_steps) ? X[(int64_t)k * m + i] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kRecBatch; ++q) {
+      const int k = k0 + q;
+      if (k > n_steps) break;
+      const bool cut = dropped && dropped[k];
+      u = cut ? r[q] / d : (r[q] + b * u) / d;
+      X[(int64_t)k * m + i] = u;
+    }
+  }
+}
+
+__global__ void copy_row_kernel(const double *src, double *dst, int m, const int *live) {
+  if (!is_live(live)) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+// b = rhs_k + [k not dropped] * C out_{k-1}  (row-form 5-slot stencil)
+__global__ void coupling_kernel(const double *rhs_k, const double *prev, double *b, pmk_stencil C,
+                                int nx, int ny, const uint8_t *dropped, int k, const int *live) {
+  if (!is_live(live)) return;
+  const int m = nx * ny;
+  const bool cut = dropped && dropped[k];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    if (cut) {
+      b[i] = rhs_k[i];
+      continue;
+    }
+    const int y = i / nx, x = i - y * nx;
+    double cs, cw, cc, ce, cn;
+    if (C.var) {
+      cs = C.coef[i];
+      cw = C.coef[m + i];
+      cc = C.coef[2 * m + i];
+      ce = C.coef[3 * m + i];
+      cn = C.coef[4 * m + i];
+    } else {
+      cs = C.c[0];
+      cw = C.c[1];
+      cc = C.c[2];
+      ce = C.c[3];
+      cn = C.c[4];
+    }
+    double acc = 0.0;
+    if (y > 0) acc = __dadd_rn(acc, __dmul_rn(cs, prev[i - nx]));
+    if (x > 0) acc = __dadd_rn(acc, __dmul_rn(cw, prev[i - 1]));
+    acc = __dadd_rn(acc, __dmul_rn(cc, prev[i]));
+    if (x < nx - 1) acc = __dadd_rn(acc, __dmul_rn(ce, prev[i + 1]));
+    if (y < ny - 1) acc = __dadd_rn(acc, __dmul_rn(cn, prev[i + nx]));
+    b[i] = __dadd_rn(rhs_k[i], acc);
+  }
+}
+
+// out = Dinv * b, one warp per row.
+__global__ void gemv_kernel(const double *__restrict__ Dinv, const double *__restrict__ b,
+                            double *__restrict__ out, int m, const int *live) {
+  if (!is_live(live)) return;
+  const int lane = threadIdx.x & 31;
+  const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (row >= m) return;
+  const double *r = Dinv + (int64_t)row * m;
+  double acc = 0.0;
+  for (int j = lane; j < m; j += 32) acc = fma(r[j], b[j], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[row] = acc;
+}
+
+}  // namespace
+
+int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
+                 cudaStream_t s) {
+  const int nx = C.nx, ny = (C.dim == 2) ? C.ny : 1;
+  const int m = nx * ny;
+  const int rows = C.n_steps + 1;
+  const int64_t N = (int64_t)rows * m;
+  (void)N;
+  if (C.kind == PMK_COARSE_DST) {
+    PMK_RETURN_IF(!C.sx || !C.delta || !C.beta || !C.work0, PMK_ERR_ARG);
+    if (ny == 1) {
+      int rc = gemm(rows, nx, nx, rhs, nx, 0, C.sx, nx, 0, C.work0, nx, 0, 1, live, s);
+      if (rc) return rc;
+      dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta, C.dropped,
+                                                           C.n_steps, m, live);
+      PMK_LAUNCH_CHECK();
+      rc = gemm(rows, nx, nx, C.work0, nx, 0, C.sx, nx, 0, out, nx, 0, 1, live, s);
+      if (rc) return rc;
+    } else {
+      PMK_RETURN_IF(!C.sy || !C.work1, PMK_ERR_ARG);
+      // X S_x over all (slice, y) rows
+      int rc = gemm(rows * ny, nx, nx, rhs, nx, 0, C.sx, nx, 0, C.work0, nx, 0, 1, live, s);
+      if (rc) return rc;
+      // S_y X_k per slice
+      rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work0, nx, m, C.work1, nx, m, rows, live, s);
+      if (rc) return rc;
+      dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta, C.dropped,
+                                                           C.n_steps, m, live);
+      PMK_LAUNCH_CHECK();
+      rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work1, nx, m, C.work0, nx, m, rows, live, s);
+      if (rc) return rc;
+      rc = gemm(rows * ny, nx, nx, C.work0, nx, 0, C.sx, nx, 0, out, nx, 0, 1, live, s);
+      if (rc) return rc;
+    }
+    // out_0 = rhs_0 exactly (stepper.py:118)
+    copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);
+    PMK_LAUNCH_CHECK();
+    return 0;
+  }
+  if (C.kind == PMK_COARSE_DENSE) {
+    PMK_RETURN_IF(!C.dinv || !C.work0, PMK_ERR_ARG);
+    copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);
+    PMK_LAUNCH_CHECK();
+    const int cb = (m + 255) / 256 < 4 * kSMs ? (m + 255) / 256 : 4 * kSMs;
+    const int gb = (m * 32 + 255) / 256;
+    for (int k = 1; k <= C.n_steps; ++k) {
+      coupling_kernel<<<cb, 256, 0, s>>>(rhs + (int64_t)k * m, out + (int64_t)(k - 1) * m,
+                                         C.work0, C.coupling, nx, ny, C.dropped, k, live);
+      PMK_LAUNCH_CHECK();
+      gemv_kernel<<<gb, 256, 0, s>>>(C.dinv, C.work0, out + (int64_t)k * m, m, live);
+      PMK_LAUNCH_CHECK();
+    }
+    return 0;
+  }
+  return PMK_ERR_UNSUPPORTED;
+}
+
+}  // namespace pmk

@@ -1,0 +1,168 @@
+// pmk_internal.cuh -- shared device helpers and launcher declarations.
+//
+// All arithmetic is fp64.  Where the reference performs a separately rounded
+// multiply and add (numpy / scipy compiled without FMA contraction), the
+// kernels use __dmul_rn / __dadd_rn / __dsub_rn explicitly, and the
+// translation units on the solver path are compiled with -fmad=false, so the
+// only rounding differences left against the reference are the reductions
+// (np.dot / OpenBLAS order) and the coarsest direct solve.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/pintmk_b200.h"
+
+namespace pmk {
+
+constexpr int kSMs = 148;
+// Fixed grid of every elementwise reduction kernel: deterministic partial
+// count independent of the vector length.
+constexpr int kRedBlocks = 4 * kSMs;  // 592
+constexpr int kRedThreads = 256;
+// Upper bound on partial sums produced by any reduction-carrying launch.
+constexpr int kMaxPartials = 8 * kSMs;  // 1184
+
+#define PMK_RETURN_IF(cond, code) \
+  do {                            \
+    if (cond) return (code);      \
+  } while (0)
+
+#define PMK_CUDA_TRY(expr)                      \
+  do {                                          \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) return (int)_e;      \
+  } while (0)
+
+#define PMK_LAUNCH_CHECK() PMK_CUDA_TRY(cudaGetLastError())
+
+// Opt-in bounds checks (make BOUNDS=1): print the offending index and trap.
+#ifdef PMK_BOUNDS
+#define PMK_CHECK_IDX(i, n, tag)                                                           \
+  do {                                                                                     \
+    if ((long long)(i) < 0 || (long long)(i) >= (long long)(n)) {                          \
+      printf("PMK OOB %s idx %lld n %lld block %d thread %d\n", tag, (long long)(i),      \
+             (long long)(n), (int)blockIdx.x, (int)threadIdx.x);                           \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define PMK_CHECK_IDX(i, n, tag) \
+  do {                           \
+  } while (0)
+#endif
+
+__device__ __forceinline__ bool is_live(const int *live) {
+  return live == nullptr || *live != 0;
+}
+
+// Deterministic block reduction: warp xor-tree, then warp 0 over the warp
+// sums.  Every block running this on the same inputs gets the same bits.
+// blockDim.x must be a multiple of 32 (<= 1024).
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();  // protect sh against a previous call
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (warp == 0) {
+    r = (lane < nw) ? sh[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+  }
+  return r;  // valid in warp 0
+}
+
+// Sum of `n` partials in a fixed order; every calling block obtains the same
+// value (broadcast through shared memory) provided blockDim.x is the same.
+__device__ __forceinline__ double reduce_partials(const double *partials, int n) {
+  __shared__ double res;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc = __dadd_rn(acc, partials[i]);
+  double s = block_sum(acc);
+  if (threadIdx.x == 0) res = s;
+  __syncthreads();
+  return res;
+}
+
+// ------------------------------------------------------------ accounting
+// RAII bracket around one kernel launch: counts it and, while profiling is
+// on, records a CUDA event pair plus the launch's algorithmic bytes/flops.
+namespace prof {
+enum Cat {
+  kMV = 0,    // plain space-time matvec
+  kMVR,       // matvec + shift + restrict
+  kIMV,       // interpolate + subtract + matvec (+ dot)
+  kMGS,       // fused MGS pass
+  kRed,       // stand-alone reductions
+  kSmall,     // begin / finish_col / backsolve (single block)
+  kAsm,       // solution assembly
+  kGemm,      // coarsest sine-transform GEMMs
+  kRec,       // coarsest per-mode recurrence
+  kCoarseMisc,// coarsest dense chain / row copy
+  kXfer,      // stand-alone restrict / interpolate / agglomeration gather
+  kNumCat
+};
+struct Scope {
+  Scope(int cat, double bytes, double flops, cudaStream_t s);
+  ~Scope();
+  int rec;
+  cudaStream_t stream;
+};
+}  // namespace prof
+
+// ------------------------------------------------------------------ march
+// Parameters of the fused space-time stencil kernels (pmk_march.cu).
+enum MarchMode { kModeMV = 0, kModeMVR = 1, kModeIMV = 2 };
+
+struct MarchParams {
+  int nx, ny, m, n_steps;
+  pmk_stencil P, Q;  // P = D^T (on v_k), Q = B^T (on v_{k-1})
+  const uint8_t *dropped;
+  const double *v;        // input (raw)
+  const double *v_scale;  // device scalar divisor or nullptr
+  double *out;            // MV: out, IMV: w
+  // MVR
+  double mu;
+  int nu;
+  double *vh;  // (n_T+1, m) time-summed (fine spatial)
+  // IMV
+  const double *vt;
+  const int32_t *group_of;
+  int m_coarse;
+  double *x_out;  // optional
+  const double *v0;
+  const double *v0_scale;
+  double *partials;  // one per block (dot(w, v0))
+  const int *live;
+};
+
+// Launch one fused march.  Returns the number of partials written (IMV) via
+// *n_partials when non-null.
+int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials);
+
+// ---------------------------------------------------------------- krylov
+int launch_dot_partials(const double *a, const double *a_scale, const double *b,
+                        const double *b_scale, int64_t n, double *partials,
+                        const int *live, cudaStream_t s);
+int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *partials,
+                           cudaStream_t s);
+int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_sqrt,
+                            cudaStream_t s);
+
+// ---------------------------------------------------------------- coarse
+int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
+                 cudaStream_t s);
+
+// --------------------------------------------------------------- transfer
+int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, const int *live,
+                     cudaStream_t s);
+int launch_restrict_time(const pmk_pair &P, const double *v, double *vh, cudaStream_t s);
+int launch_interpolate(const pmk_pair &P, const double *w, double *out, cudaStream_t s);
+
+}  // namespace pmk

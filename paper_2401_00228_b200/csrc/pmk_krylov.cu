@@ -1,0 +1,334 @@
+// pmk_krylov.cu -- FGMRES building blocks on the device (reference
+// solver.py:362-456) and the stand-alone intergrid transfers
+// (intergrid.py:51-63, 106-120).
+//
+// Krylov basis vectors are stored UNNORMALISED: the reference appends
+// b / beta and w / h[j+1, j] (solver.py:395, 420); here the raw vector and
+// its divisor stay separate and every reader computes raw[i] / scale with an
+// IEEE division, which yields bitwise the values the reference stores while
+// saving a full read+write pass per iteration.
+//
+// All reductions are two-level with a fixed grid (kRedBlocks) and a fixed
+// summation order, so results are bitwise reproducible.  The second level is
+// folded into the prologue of the next consumer kernel: every block of the
+// consumer sums the same partials in the same order, so no separate reduce
+// launch and no host round trip is needed between MGS passes.
+#include <math.h>
+
+#include "pmk_internal.cuh"
+#include "pmk_krylov.cuh"
+
+namespace pmk {
+namespace {
+
+__device__ __forceinline__ double ld_scaled(const double *p, int64_t i, double sc, bool has) {
+  const double v = p[i];
+  return has ? __ddiv_rn(v, sc) : v;
+}
+
+// ------------------------------------------------------------ reductions
+__global__ void __launch_bounds__(kRedThreads)
+    dot_partials_kernel(const double *a, const double *as, const double *b, const double *bs,
+                        int64_t n, double *partials, const int *live) {
+  if (!is_live(live)) return;
+  const double sa = as ? *as : 1.0, sb = bs ? *bs : 1.0;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double x = ld_scaled(a, i, sa, as != nullptr);
+    const double y = ld_scaled(b, i, sb, bs != nullptr);
+    acc = __dadd_rn(acc, __dmul_rn(x, y));
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// partial sums of (a - b)^2 with r = a - b rounded first (stepper.py:192-193)
+__global__ void __launch_bounds__(kRedThreads)
+    diffsq_partials_kernel(const double *a, const double *b, int64_t n, double *partials) {
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = __dsub_rn(a[i], b[i]);
+    acc = __dadd_rn(acc, __dmul_rn(r, r));
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void reduce_scalar_kernel(const double *partials, int n, double *out, int do_sqrt) {
+  const double s = reduce_partials(partials, n);
+  if (threadIdx.x == 0) *out = do_sqrt ? sqrt(s) : s;
+}
+
+// ------------------------------------------------------------ fgmres state
+// begin: beta = ||b|| from the partials, init g, flags (solver.py:381-396).
+__global__ void begin_kernel(KState *st, const double *partials, int n_partials,
+                             const int *parent_live) {
+  const bool entered = is_live(parent_live);
+  const double ss = entered ? reduce_partials(partials, n_partials) : 0.0;
+  if (threadIdx.x == 0) {
+    st->entered = entered ? 1 : 0;
+    st->n_iter = 0;
+    st->breakdown = 0;
+    if (!entered) {
+      st->live = 0;
+      return;
+    }
+    const double beta = sqrt(ss);
+    st->beta = beta;
+    st->vscale[0] = beta;
+    st->g[0] = beta;
+    st->rel = 1.0;
+    st->live = (beta == 0.0) ? 0 : 1;  // solver.py:382-383: zero rhs -> x = 0
+  }
+}
+
+// One fused MGS pass (solver.py:405-408) for basis index l of column j:
+//   h[l][j] = <w, v_l>            (from the previous pass' partials)
+//   w      -= h[l][j] * v_l
+//   partial <w, v_{l+1}>          (or <w, w> on the last pass, solver.py:412)
+__global__ void __launch_bounds__(kRedThreads)
+    mgs_pass_kernel(KState *st, int ld, int l, int j, double *w, const double *vl,
+                    const double *vl_scale, const double *vn, const double *vn_scale, int64_t n,
+                    const double *prev, int n_prev, double *partials) {
+  if (!st->live) return;
+  const double h = reduce_partials(prev, n_prev);
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->h[l * ld + j] = h;
+  const double sl = vl_scale ? *vl_scale : 1.0;
+  const bool last = (vn == nullptr);
+  const double sn = (!last && vn_scale) ? *vn_scale : 1.0;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = ld_scaled(vl, i, sl, vl_scale != nullptr);
+    const double wn = __dsub_rn(w[i], __dmul_rn(h, v));
+    w[i] = wn;
+    const double z = last ? wn : ld_scaled(vn, i, sn, vn_scale != nullptr);
+    acc = __dadd_rn(acc, __dmul_rn(wn, z));
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// h[j+1][j] = ||w||, breakdown test, Givens update (solver.py:412-440).
+__global__ void finish_col_kernel(KState *st, int ld, int j, const double *partials,
+                                  int n_partials, double tol) {
+  if (!st->live) return;
+  const double ss = reduce_partials(partials, n_partials);
+  if (threadIdx.x != 0) return;
+  double *h = st->h;
+  const double hn = sqrt(ss);
+  h[(j + 1) * ld + j] = hn;
+  for (int l = 0; l <= j + 1; ++l) st->hraw[l * ld + j] = h[l * ld + j];
+  st->n_iter = j + 1;
+  double cn2 = 0.0;  // np.linalg.norm(h[:j+2, j])
+  for (int l = 0; l <= j + 1; ++l) cn2 = __dadd_rn(cn2, __dmul_rn(h[l * ld + j], h[l * ld + j]));
+  const double col_norm = sqrt(cn2);
+  const bool breakdown = hn <= 1e-14 * fmax(col_norm, 1e-300);
+  if (!breakdown) st->vscale[j + 1] = hn;
+  double *cs = st->cs, *sn = st->sn, *g = st->g;
+  for (int l = 0; l < j; ++l) {
+    const double a = h[l * ld + j], b = h[(l + 1) * ld + j];
+    const double tmp = __dadd_rn(__dmul_rn(cs[l], a), __dmul_rn(sn[l], b));
+    h[(l + 1) * ld + j] = __dadd_rn(__dmul_rn(-sn[l], a), __dmul_rn(cs[l], b));
+    h[l * ld + j] = tmp;
+  }
+  const double hjj = h[j * ld + j], hj1 = h[(j + 1) * ld + j];
+  const double denom = hypot(hjj, hj1);
+  cs[j] = __ddiv_rn(hjj, denom);
+  sn[j] = __ddiv_rn(hj1, denom);
+  h[j * ld + j] = denom;
+  h[(j + 1) * ld + j] = 0.0;
+  g[j + 1] = __dmul_rn(-sn[j], g[j]);
+  g[j] = __dmul_rn(cs[j], g[j]);
+  const double rel = __ddiv_rn(fabs(g[j + 1]), st->beta);
+  st->rel = rel;
+  st->hist[j] = rel;
+  if (breakdown) {
+    st->breakdown = 1;
+    st->live = 0;
+  } else if (tol > 0.0 && rel <= tol) {
+    st->live = 0;  // converged (solver.py:438-440)
+  }
+}
+
+// Back substitution (solver.py:442-444).
+__global__ void backsolve_kernel(KState *st, int ld) {
+  if (!st->entered || threadIdx.x != 0) return;
+  const int n = st->n_iter;
+  const double *h = st->h, *g = st->g;
+  double *y = st->y;
+  for (int i = n - 1; i >= 0; --i) {
+    double d = 0.0;
+    for (int k = i + 1; k < n; ++k) d = __dadd_rn(d, __dmul_rn(h[i * ld + k], y[k]));
+    y[i] = __ddiv_rn(__dsub_rn(g[i], d), h[i * ld + i]);
+  }
+}
+
+// x = sum_i y_i x_i with x_i = v_i - Z vt_i recomputed (solver.py:445-447,
+// 359).  `first` > 0 continues an accumulation already in x.
+__global__ void __launch_bounds__(256)
+    assemble_kernel(const KState *st, AssembleArgs a, double *x, int64_t n, int m, int nu,
+                    int m_coarse, const int32_t *group_of, int first) {
+  if (!st->entered) return;
+  const int n_iter = st->n_iter;
+  const int hi = min(n_iter, first + a.count);
+  if (first > 0 && first >= n_iter) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / m;
+    const int64_t i = e - k * m;
+    const int64_t K = (k == 0) ? 0 : (k - 1) / nu + 1;
+    const int64_t ci = K * m_coarse + (group_of ? (int64_t)group_of[i] : i);
+    double acc = (first == 0) ? 0.0 : x[e];
+    for (int l = first; l < hi; ++l) {
+      const int q = l - first;
+      const double v = __ddiv_rn(a.vraw[q][e], st->vscale[l]);
+      const double xl = __dsub_rn(v, a.vt[q][ci]);
+      acc = __dadd_rn(acc, __dmul_rn(st->y[l], xl));
+    }
+    x[e] = acc;
+  }
+}
+
+// ------------------------------------------------------------- transfers
+__global__ void restrict_time_kernel(const double *v, double *vh, int nu, int n_T, int m) {
+  const int64_t total = (int64_t)(n_T + 1) * m;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t K = e / m, i = e - K * m;
+    if (K == 0) {
+      vh[e] = v[i];
+    } else {
+      const int64_t base = ((K - 1) * nu + 1) * m + i;
+      double acc = v[base];
+      for (int q = 1; q < nu; ++q) acc = __dadd_rn(acc, v[base + (int64_t)q * m]);
+      vh[e] = acc;
+    }
+  }
+}
+
+// Y^T gather: out[K, c] = sum_{j in group c, ascending} Y[j, c] * fine[K, j]
+// (the csc_matvecs order of `summed @ y_space`, intergrid.py:109-111).
+__global__ void ts_gather_kernel(const double *fine, double *coarse, const int32_t *ptr,
+                                 const int32_t *idx, const double *val, int n_rows, int m_fine,
+                                 int m_coarse, const int *live) {
+  if (!is_live(live)) return;
+  const int64_t total = (int64_t)n_rows * m_coarse;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t K = e / m_coarse;
+    const int c = (int)(e - K * m_coarse);
+    const double *row = fine + K * m_fine;
+    double acc = 0.0;
+    for (int q = ptr[c]; q < ptr[c + 1]; ++q) acc = __dadd_rn(acc, __dmul_rn(val[q], row[idx[q]]));
+    coarse[e] = acc;
+  }
+}
+
+__global__ void interpolate_kernel(const double *w, double *out, int nu, int n_T, int m_fine,
+                                   int m_coarse, const int32_t *group_of) {
+  const int64_t total = (int64_t)(nu * n_T + 1) * m_fine;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / m_fine, i = e - k * m_fine;
+    const int64_t K = (k == 0) ? 0 : (k - 1) / nu + 1;
+    out[e] = w[K * m_coarse + (group_of ? (int64_t)group_of[i] : i)];
+  }
+}
+
+int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > 16 * kSMs) g = 16 * kSMs;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ launchers
+int launch_dot_partials(const double *a, const double *a_scale, const double *b,
+                        const double *b_scale, int64_t n, double *partials, const int *live,
+                        cudaStream_t s) {
+  dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, a_scale, b, b_scale, n, partials,
+                                                         live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *partials,
+                           cudaStream_t s) {
+  diffsq_partials_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, partials);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_sqrt,
+                            cudaStream_t s) {
+  reduce_scalar_kernel<<<1, kRedThreads, 0, s>>>(partials, n, out, do_sqrt);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
+                 cudaStream_t s) {
+  begin_kernel<<<1, kRedThreads, 0, s>>>(st, partials, n_partials, parent_live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *vl,
+                    const double *vl_scale, const double *vn, const double *vn_scale, int64_t n,
+                    const double *prev, int n_prev, double *partials, cudaStream_t s) {
+  mgs_pass_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, l, j, w, vl, vl_scale, vn, vn_scale,
+                                                     n, prev, n_prev, partials);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
+                      double tol, cudaStream_t s) {
+  finish_col_kernel<<<1, kRedThreads, 0, s>>>(st, ld, j, partials, n_partials, tol);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_backsolve(KState *st, int ld, cudaStream_t s) {
+  backsolve_kernel<<<1, 32, 0, s>>>(st, ld);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t n, int m, int nu,
+                    int m_coarse, const int32_t *group_of, int first, cudaStream_t s) {
+  assemble_kernel<<<grid_for(n, 256), 256, 0, s>>>(st, a, x, n, m, nu, m_coarse, group_of, first);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_restrict_time(const pmk_pair &P, const double *v, double *vh, cudaStream_t s) {
+  const int64_t n = (int64_t)(P.n_T + 1) * P.m_fine;
+  restrict_time_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, vh, P.nu, P.n_T, P.m_fine);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, const int *live,
+                     cudaStream_t s) {
+  const int64_t n = (int64_t)(P.n_T + 1) * P.m_coarse;
+  ts_gather_kernel<<<grid_for(n, 256), 256, 0, s>>>(fine, coarse, P.y_ptr, P.y_idx, P.y_val,
+                                                    P.n_T + 1, P.m_fine, P.m_coarse, live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_interpolate(const pmk_pair &P, const double *w, double *out, cudaStream_t s) {
+  const int64_t n = (int64_t)(P.nu * P.n_T + 1) * P.m_fine;
+  interpolate_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, out, P.nu, P.n_T, P.m_fine, P.m_coarse,
+                                                      P.group_of);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+}  // namespace pmk

@@ -1,0 +1,43 @@
+// pmk_krylov.cuh -- device-resident FGMRES state and launchers.
+#pragma once
+
+#include "pmk_internal.cuh"
+
+namespace pmk {
+
+// Device-resident state of one fgmres invocation (solver.py:389-396).
+// The header lives in device memory so that every kernel of the iteration
+// (including the ones captured in CUDA graphs) reads and updates it without
+// host involvement.
+struct KState {
+  double *h;     // (cap+1) x cap, row-major, ld = cap; rotated in place
+  double *hraw;  // unrotated copy (keep_basis, tests)
+  double *cs, *sn, *g, *y;
+  double *vscale;  // vscale[l]: divisor of raw basis vector l (beta, h[l][l-1])
+  double *hist;    // residual history rel_j
+  double beta, rel;
+  int live;      // iterating (cleared on breakdown / convergence / beta == 0)
+  int entered;   // parent was live when this invocation began
+  int n_iter;
+  int breakdown;
+};
+
+constexpr int kAsmChunk = 32;
+struct AssembleArgs {
+  int count;
+  const double *vraw[kAsmChunk];
+  const double *vt[kAsmChunk];
+};
+
+int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
+                 cudaStream_t s);
+int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *vl,
+                    const double *vl_scale, const double *vn, const double *vn_scale, int64_t n,
+                    const double *prev, int n_prev, double *partials, cudaStream_t s);
+int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
+                      double tol, cudaStream_t s);
+int launch_backsolve(KState *st, int ld, cudaStream_t s);
+int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t n, int m, int nu,
+                    int m_coarse, const int32_t *group_of, int first, cudaStream_t s);
+
+}  // namespace pmk

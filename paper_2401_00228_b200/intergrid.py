@@ -1,0 +1,215 @@
+"""Intergrid pairs and coarse systems on the GPU.
+
+Mirror of reference ``pintmk/intergrid.py`` for the families on the MLK hot
+path: pure time coarsening (TimePair, Y = Z = nu-fold identity stacks) and
+simultaneous time-space coarsening by agglomeration (TimeSpacePair, Z
+piecewise-constant injection, Y agglomerate averaging), plus the perturbed
+decoupling of the coarsest level.  The MGRIT reduction pair is not on this
+path (SURVEY.md section 8(f) lists it as the next row).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from .stepper import BlockBidiagonalSystem, StepOperators, _back, _to_device
+
+
+class CoarseSystem(BlockBidiagonalSystem):
+    """Block bidiagonal coarse matrix tagged with its provenance (reference
+    intergrid.py:24-30)."""
+
+    def __init__(self, diag, sub, n_steps, provenance: str, dropped: tuple[int, ...] = (),
+                 grid=None, dim=None, spectral=None):
+        super().__init__(diag, sub, n_steps, dropped=dropped, grid=grid, dim=dim,
+                         spectral=spectral)
+        self.provenance = provenance
+
+
+class _PairBase:
+    fine_rows: int
+    n_T: int
+    nu: int
+
+    def _pair_desc(self) -> _lib.PairDesc:
+        raise NotImplementedError
+
+    def restrict(self, v):
+        """Y^T v (sum over each slab's nu rows; averaging for space pairs)."""
+        torch = _lib.require_cuda()
+        shape = tuple(v.shape) if hasattr(v, "shape") else np.shape(v)
+        dv, was_np = _to_device(v)
+        if dv.numel() != self.fine_rows * self.n:
+            raise ValueError("vector size does not match the fine level")
+        out = torch.empty((self.n_T + 1) * self.m, dtype=torch.float64, device="cuda")
+        scratch = None
+        if self.m != self.n or getattr(self, "partition", None) is not None:
+            scratch = torch.empty((self.n_T + 1) * self.n, dtype=torch.float64, device="cuda")
+        lib = _lib.load()
+        _lib.check(lib.pmk_restrict(ctypes.byref(self._pair_desc()), _lib.ptr(dv), _lib.ptr(out),
+                                    _lib.ptr(scratch), _lib.stream_ptr()), "restrict")
+        return _back(out, was_np, (-1,) if len(shape) == 1 else (self.n_T + 1, self.m))
+
+    def interpolate(self, w):
+        """Z w (repeat each coarse row nu times; injection for space pairs)."""
+        torch = _lib.require_cuda()
+        shape = tuple(w.shape) if hasattr(w, "shape") else np.shape(w)
+        dw, was_np = _to_device(w)
+        if dw.numel() != (self.n_T + 1) * self.m:
+            raise ValueError("vector size does not match the coarse level")
+        out = torch.empty(self.fine_rows * self.n, dtype=torch.float64, device="cuda")
+        lib = _lib.load()
+        _lib.check(lib.pmk_interpolate(ctypes.byref(self._pair_desc()), _lib.ptr(dw),
+                                       _lib.ptr(out), _lib.stream_ptr()), "interpolate")
+        return _back(out, was_np, (-1,) if len(shape) == 1 else (self.fine_rows, self.n))
+
+
+class TimePair(_PairBase):
+    """Pure time coarsening (reference intergrid.py:37-76)."""
+
+    kind = "T"
+    partition = None
+
+    def __init__(self, n: int, nu: int, n_T: int):
+        if nu < 1:
+            raise ValueError("nu must be positive")
+        self.n = n
+        self.m = n
+        self.nu = nu
+        self.n_T = n_T
+        self.fine_rows = nu * n_T + 1
+        self._desc = None
+
+    def _pair_desc(self) -> _lib.PairDesc:
+        if self._desc is None:
+            d = _lib.PairDesc()
+            d.nu, d.n_T, d.m_fine, d.m_coarse = self.nu, self.n_T, self.n, self.n
+            d.group_of = d.y_ptr = d.y_idx = d.y_val = None
+            self._desc = d
+        return self._desc
+
+    def block_matrices(self, k: int):
+        """(Y_k, Z_k) for one slab (identical here)."""
+        eye = sp.identity(self.n, format="csr")
+        z = eye if k == 0 else sp.vstack([eye] * self.nu, format="csr")
+        return z, z
+
+    def materialize(self):
+        z = sp.block_diag([self.block_matrices(k)[1] for k in range(self.n_T + 1)], format="csr")
+        return z, z
+
+
+class TimeSpacePair(_PairBase):
+    """Time and space coarsening by agglomeration (reference
+    intergrid.py:79-131); nu = 1 gives the pure space move."""
+
+    kind = "TS"
+
+    def __init__(self, nu: int, n_T: int, partition: list[np.ndarray], n: int):
+        if nu < 1:
+            raise ValueError("nu must be positive")
+        sizes = np.array([len(g) for g in partition])
+        if sizes.min() == 0:
+            raise ValueError("empty agglomerate")
+        flat = np.concatenate(partition)
+        if len(np.unique(flat)) != n or len(flat) != n:
+            raise ValueError("partition must cover all indices exactly once")
+        self.nu = nu
+        self.n_T = n_T
+        self.n = n
+        self.m = len(partition)
+        self.partition = partition
+        self.fine_rows = nu * n_T + 1
+        cols = np.repeat(np.arange(self.m), sizes)
+        self.z_space = sp.csr_matrix((np.ones(n), (flat, cols)), shape=(n, self.m))
+        self.y_space = sp.csr_matrix((np.repeat(1.0 / sizes, sizes), (flat, cols)),
+                                     shape=(n, self.m))
+        self._desc = None
+        self._keep = []
+
+    def _pair_desc(self) -> _lib.PairDesc:
+        if self._desc is None:
+            torch = _lib.require_cuda()
+            group_of = np.empty(self.n, dtype=np.int32)
+            for c, g in enumerate(self.partition):
+                group_of[np.asarray(g)] = c
+            yt = sp.csr_matrix(self.y_space.T)
+            yt.sort_indices()
+            tabs = [torch.from_numpy(group_of).cuda(),
+                    torch.from_numpy(yt.indptr.astype(np.int32)).cuda(),
+                    torch.from_numpy(yt.indices.astype(np.int32)).cuda(),
+                    torch.from_numpy(yt.data.astype(np.float64)).cuda()]
+            self._keep = tabs
+            d = _lib.PairDesc()
+            d.nu, d.n_T, d.m_fine, d.m_coarse = self.nu, self.n_T, self.n, self.m
+            d.group_of, d.y_ptr, d.y_idx, d.y_val = (t.data_ptr() for t in tabs)
+            self._desc = d
+        return self._desc
+
+    def block_matrices(self, k: int):
+        if k == 0:
+            return self.y_space, self.z_space
+        return (sp.vstack([self.y_space] * self.nu, format="csr"),
+                sp.vstack([self.z_space] * self.nu, format="csr"))
+
+    def materialize(self):
+        ys, zs = zip(*(self.block_matrices(k) for k in range(self.n_T + 1)))
+        return sp.block_diag(ys, format="csr"), sp.block_diag(zs, format="csr")
+
+
+def build_t_pair(n: int, nu: int, n_T: int) -> TimePair:
+    return TimePair(n, nu, n_T)
+
+
+def build_ts_pair(n: int, nu: int, n_T: int, partition) -> TimeSpacePair:
+    return TimeSpacePair(nu=nu, n_T=n_T, partition=list(partition), n=n)
+
+
+def agglomerate_partition(n_x: int, n_y: int = 1):
+    """Factor-2 agglomeration per direction, leftovers joining the last group
+    (reference intergrid.py:202-227).  Returns (groups, (m_x, m_y)) with the
+    groups in row-major coarse order."""
+    def spans(count: int):
+        half = count // 2
+        if half == 0:
+            raise ValueError("grid too small to agglomerate")
+        bounds = [(2 * i, 2 * i + 2) for i in range(half)]
+        bounds[-1] = (bounds[-1][0], count)
+        return bounds
+
+    xs = spans(n_x)
+    if n_y == 1:
+        return [np.arange(a, b) for a, b in xs], (len(xs), 1)
+    ys = spans(n_y)
+    groups = []
+    for ya, yb in ys:
+        for xa, xb in xs:
+            iy, ix = np.meshgrid(np.arange(ya, yb), np.arange(xa, xb), indexing="ij")
+            groups.append((iy * n_x + ix).ravel())
+    return groups, (len(xs), len(ys))
+
+
+def closed_form_t_coarse(ops: StepOperators, nu: int, n_T: int) -> CoarseSystem:
+    """Time-coarsened Galerkin system in closed form (reference
+    intergrid.py:243-255)."""
+    cfg = ops.config
+    eye = sp.identity(ops.n, format="csr")
+    diag = (eye - (nu - 1 + cfg.theta) * cfg.delta_t * ops.spatial.matrix).tocsr()
+    sub = (eye + (1 - cfg.theta) * cfg.delta_t * ops.spatial.matrix).tocsr()
+    return CoarseSystem(diag=diag, sub=sub, n_steps=n_T, provenance="closed_form",
+                        grid=ops.spatial.grid, dim=ops.spatial.dim)
+
+
+def perturb_decouple(cs: CoarseSystem, n_cgs: int) -> CoarseSystem:
+    """Drop the couplings at balanced chunk starts (reference
+    intergrid.py:299-311); n_cgs >= n_T makes the system block diagonal."""
+    if not 1 <= n_cgs <= cs.n_steps + 1:
+        raise ValueError(f"n_cgs must be in [1, {cs.n_steps + 1}]")
+    chunks = np.array_split(np.arange(1, cs.n_steps + 1), min(n_cgs, cs.n_steps))
+    dropped = tuple(int(c[0]) for c in chunks if len(c))
+    return CoarseSystem(diag=cs.diag, sub=cs.sub, n_steps=cs.n_steps, provenance="perturbed",
+                        dropped=dropped, grid=cs.grid, dim=cs.dim, spectral=cs.spectral)

@@ -1,0 +1,546 @@
+"""FGMRES with the multilevel Krylov (MLK) shift preconditioner, on one B200.
+
+Mirror of reference ``pintmk/solver.py`` (names, arguments, error
+behaviour).  The hierarchy is built on the host exactly as the reference
+builds it; the solve runs on the device:
+
+* the outer FGMRES (level 0) is driven from Python one iteration at a time
+  (one small device->host read per iteration for the stop test,
+  solver.py:433-440);
+* each iteration is a handful of fused sm_100a kernels (shift+restrict,
+  interpolate+subtract+matvec, fused MGS passes, device-side Givens) plus
+  the inner recursion, which runs entirely in native code with no host
+  synchronisation (solver.py:347-348);
+* the coarsest level is a sine-diagonalised or dense direct solve.
+
+Extensions over the reference (default-off): ``SolverConfig.restart``
+(FGMRES(m)), the ``"time_space"`` schedule move (reference _space_move with
+time_nu = nu, solver.py:127-143).  ``ledger``/``model`` (simulated-parallel
+cost accounting, parcost.py) are accepted and ignored: the GPU measures
+real time.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _lib
+from ._device import SpectralInfo
+from .intergrid import (CoarseSystem, TimePair, TimeSpacePair, agglomerate_partition,
+                        perturb_decouple)
+from .spatial import gershgorin_bound
+from .stepper import BlockBidiagonalSystem, FineSystem, _to_device
+
+
+@dataclass
+class SolveReport:
+    """Outcome of one iterative solve (reference reports.py:8-25)."""
+
+    method: str
+    outer_iterations: int = 0
+    residual_history: list[float] = field(default_factory=list)
+    converged: bool = False
+    tol: float = 0.0
+    error_vs_oracle: float | None = None
+    wall_time: float | None = None
+    simulated_elapsed: int | None = None
+    level_stats: dict = field(default_factory=dict)
+    metadata: dict = field(default_factory=dict)
+
+    @property
+    def final_residual(self) -> float:
+        return self.residual_history[-1] if self.residual_history else float("inf")
+
+
+@dataclass
+class SolverConfig:
+    """Krylov knobs (reference solver.py:37-57) plus ``restart``.
+
+    ``basis_memory_limit``/``basis_dir`` are accepted for compatibility: the
+    device keeps the basis in HBM (no disk spill); ``restart`` bounds it.
+    """
+
+    mu: float = 1.0
+    tol: float = 1e-6
+    max_outer: int = 200
+    inner_iters: int | list[int] | None = None
+    coarsest_n_cgs: int = 0
+    basis_memory_limit: int = 2 * 1024**3
+    basis_dir: str | None = None
+    restart: int | None = None
+
+    def __post_init__(self):
+        if self.mu == 0:
+            raise ValueError("mu must be nonzero")
+        if self.restart is not None and self.restart < 1:
+            raise ValueError("restart must be >= 1")
+
+
+@dataclass(eq=False)
+class Level:
+    """One rung of the hierarchy (reference solver.py:60-81)."""
+
+    system: BlockBidiagonalSystem
+    spatial_matrix: sp.csr_matrix
+    dt: float
+    implicit_weight: float
+    n_steps: int
+    grid: tuple[int, int]
+    dim: int
+    kind: str
+    pair: object | None = None
+    budget: int = 0
+    laplace_factor: float | None = None  # set while spatial_matrix is the pristine Laplacian
+
+    @property
+    def state_dim(self) -> int:
+        return self.spatial_matrix.shape[0]
+
+    @property
+    def total_dim(self) -> int:
+        return (self.n_steps + 1) * self.state_dim
+
+
+class LevelHierarchy:
+    """Levels, fine system, config, and the native solver state."""
+
+    def __init__(self, levels: list[Level], fine: FineSystem, config: SolverConfig):
+        self.levels = levels
+        self.fine = fine
+        self.config = config
+        self.moves: list[str] = []
+        self._native = None
+        self._buffers: list = []
+
+    @property
+    def n_levels(self) -> int:
+        return len(self.levels)
+
+    def describe(self) -> list[dict]:
+        return [{"kind": lv.kind, "n_steps": lv.n_steps, "grid": lv.grid, "dt": lv.dt,
+                 "implicit_weight": lv.implicit_weight, "budget": lv.budget}
+                for lv in self.levels]
+
+    def __del__(self):
+        if self._native:
+            try:
+                _lib.load().pmk_hier_destroy(self._native)
+            except Exception:
+                pass
+            self._native = None
+
+
+# ------------------------------------------------------------- construction
+def _coarse_system_from(spatial_matrix, implicit_weight, dt, n_steps, grid, dim,
+                        laplace_factor) -> CoarseSystem:
+    """D = I - a dt A, B = I + (1-a) dt A (reference solver.py:105-110)."""
+    eye = sp.identity(spatial_matrix.shape[0], format="csr")
+    diag = (eye - implicit_weight * dt * spatial_matrix).tocsr()
+    sub = (eye + (1.0 - implicit_weight) * dt * spatial_matrix).tocsr()
+    spectral = None
+    if laplace_factor is not None:
+        spectral = SpectralInfo(laplace_factor, implicit_weight * dt,
+                                (1.0 - implicit_weight) * dt)
+    return CoarseSystem(diag=diag, sub=sub, n_steps=n_steps, provenance="closed_form",
+                        grid=grid, dim=dim, spectral=spectral)
+
+
+def _time_move(level: Level, nu: int) -> Level:
+    """Time coarsening by nu (reference solver.py:113-124)."""
+    if level.n_steps % nu != 0:
+        raise ValueError(f"time move needs nu | n_steps, got {level.n_steps} / {nu}")
+    level.pair = TimePair(level.state_dim, nu, level.n_steps // nu)
+    a = 1.0 - (1.0 - level.implicit_weight) / nu
+    dt = nu * level.dt
+    n_steps = level.n_steps // nu
+    system = _coarse_system_from(level.spatial_matrix, a, dt, n_steps, level.grid, level.dim,
+                                 level.laplace_factor)
+    return Level(system=system, spatial_matrix=level.spatial_matrix, dt=dt, implicit_weight=a,
+                 n_steps=n_steps, grid=level.grid, dim=level.dim, kind="time",
+                 laplace_factor=level.laplace_factor)
+
+
+def _space_move(level: Level, time_nu: int = 1) -> Level:
+    """Agglomeration in space, optionally with time coarsening (reference
+    solver.py:127-143)."""
+    gx, gy = level.grid
+    groups, (mx, my) = agglomerate_partition(gx, gy if level.dim == 2 else 1)
+    if level.n_steps % time_nu != 0:
+        raise ValueError("time factor must divide n_steps")
+    n_steps = level.n_steps // time_nu
+    pair = TimeSpacePair(nu=time_nu, n_T=n_steps, partition=groups, n=level.state_dim)
+    level.pair = pair
+    coarse_a = (pair.y_space.T @ level.spatial_matrix @ pair.z_space).tocsr()
+    a = 1.0 - (1.0 - level.implicit_weight) / time_nu
+    dt = time_nu * level.dt
+    system = _coarse_system_from(coarse_a, a, dt, n_steps, (mx, my), level.dim, None)
+    return Level(system=system, spatial_matrix=coarse_a, dt=dt, implicit_weight=a,
+                 n_steps=n_steps, grid=(mx, my), dim=level.dim,
+                 kind="space" if time_nu == 1 else "time_space")
+
+
+def _fine_level(fine: FineSystem) -> Level:
+    ops = fine.ops
+    sp_op = ops.spatial
+    return Level(system=fine, spatial_matrix=sp_op.matrix, dt=ops.config.delta_t,
+                 implicit_weight=ops.config.theta, n_steps=fine.n_t,
+                 grid=(sp_op.n_x, sp_op.n_y), dim=sp_op.dim, kind="fine",
+                 laplace_factor=sp_op.tau / sp_op.delta_x**2)
+
+
+def time_move_is_stable(level: Level, nu: int = 2) -> bool:
+    """Stability screen of a prospective time move (reference solver.py:154-163)."""
+    explicit = (1.0 - level.implicit_weight) / nu
+    lam = gershgorin_bound(level.spatial_matrix) / level.dim
+    return (1.0 - 2.0 * explicit) * (nu * level.dt) * lam <= 2.0
+
+
+def auto_moves_step(level: Level, alternating: bool, next_is_space: bool, nu: int = 2):
+    """Next automatic move (reference solver.py:166-175)."""
+    if not alternating:
+        if level.n_steps % nu == 0 and time_move_is_stable(level, nu):
+            return "time", False, False
+        alternating = True
+        next_is_space = True
+    return ("space" if next_is_space else "time"), True, not next_is_space
+
+
+def _assign_budgets(levels: list[Level], inner_iters) -> None:
+    """Inner FGMRES budgets (reference solver.py:219-235)."""
+    inter = levels[1:-1]
+    if not inter:
+        return
+    if inner_iters is None:
+        budgets = [2] * len(inter)
+        if len(budgets) > 1:
+            budgets[-1] = 1
+    elif isinstance(inner_iters, int):
+        budgets = [inner_iters] * len(inter)
+    else:
+        budgets = list(inner_iters)
+        if len(budgets) != len(inter):
+            raise ValueError("need one inner budget per intermediate level")
+    for lvl, b in zip(inter, budgets):
+        if b < 1:
+            raise ValueError("budgets must be >= 1")
+        lvl.budget = b
+
+
+def build_hierarchy(fine: FineSystem, n_levels: int, schedule: str | list[str] = "auto",
+                    cfg: SolverConfig | None = None, nu: int = 2) -> LevelHierarchy:
+    """Level stack by repeated coarsening (reference solver.py:178-216).
+
+    Moves: "time", "space" (reference) and "time_space" (agglomeration plus
+    time coarsening by nu in one move).
+    """
+    cfg = cfg or SolverConfig()
+    if n_levels < 2:
+        raise ValueError("need at least two levels")
+    levels = [_fine_level(fine)]
+    moves: list[str] = []
+    alternating = False
+    next_is_space = False
+    for i in range(n_levels - 1):
+        cur = levels[-1]
+        if schedule == "auto":
+            move, alternating, next_is_space = auto_moves_step(cur, alternating, next_is_space,
+                                                               nu)
+        else:
+            move = schedule[i]
+        if move == "time":
+            levels.append(_time_move(cur, nu))
+        elif move == "space":
+            levels.append(_space_move(cur))
+        elif move == "time_space":
+            levels.append(_space_move(cur, time_nu=nu))
+        else:
+            raise ValueError(f"unknown move {move!r}")
+        moves.append(move)
+    _assign_budgets(levels, cfg.inner_iters)
+    if cfg.coarsest_n_cgs >= 1:
+        levels[-1].system = perturb_decouple(levels[-1].system, cfg.coarsest_n_cgs)
+    hier = LevelHierarchy(levels=levels, fine=fine, config=cfg)
+    hier.moves = moves
+    _setup_native(hier)
+    return hier
+
+
+def build_two_level(fine: FineSystem, family: str, nu: int,
+                    cfg: SolverConfig | None = None) -> LevelHierarchy:
+    """Two-level hierarchy for the T or TS family (reference solver.py:238-265).
+    The MGRIT family is not on this path yet."""
+    cfg = cfg or SolverConfig()
+    top = _fine_level(fine)
+    if family == "T":
+        coarse = _time_move(top, nu)
+    elif family == "TS":
+        coarse = _space_move(top, time_nu=nu)
+    elif family == "MGRIT":
+        raise NotImplementedError("MGRIT intergrid family is not implemented on the GPU path")
+    else:
+        raise ValueError(f"unknown family {family!r}")
+    if cfg.coarsest_n_cgs >= 1:
+        coarse.system = perturb_decouple(coarse.system, cfg.coarsest_n_cgs)
+    hier = LevelHierarchy(levels=[top, coarse], fine=fine, config=cfg)
+    hier.moves = [family]
+    _setup_native(hier)
+    return hier
+
+
+def _empty(n):
+    import torch
+
+    return torch.empty(n, dtype=torch.float64, device="cuda")
+
+
+def _setup_native(hier: LevelHierarchy) -> None:
+    """Register levels, pairs, budgets, the coarsest solver and the inner
+    workspaces with the native runtime (prefactor, solver.py:213)."""
+    _lib.require_cuda()
+    lib = _lib.load()
+    L = hier.n_levels
+    H = lib.pmk_hier_create(L, float(hier.config.mu))
+    if not H:
+        raise RuntimeError("pmk_hier_create failed")
+    hier._native = H
+    keep = hier._buffers
+    for idx in range(L - 1):
+        lvl = hier.levels[idx]
+        pdesc = lvl.pair._pair_desc()
+        _lib.check(lib.pmk_hier_set_level(H, idx, ctypes.byref(lvl.system.level_desc()),
+                                          ctypes.byref(pdesc), int(lvl.budget)), "set_level")
+    coarse = hier.levels[-1].system.diag_factorization
+    keep.append(coarse)
+    _lib.check(lib.pmk_hier_set_coarse(H, ctypes.byref(coarse.desc)), "set_coarse")
+    for idx in range(L - 1):
+        lvl = hier.levels[idx]
+        nxt = hier.levels[idx + 1]
+        ts = None
+        if isinstance(lvl.pair, TimeSpacePair):
+            ts = _empty((lvl.pair.n_T + 1) * lvl.pair.n)
+        if idx == 0:
+            rhs = hier.fine.rhs.reshape(-1)
+            ws, cos = [], []
+        else:
+            rhs = _empty(lvl.total_dim)
+            ws = [_empty(lvl.total_dim) for _ in range(lvl.budget)]
+            cos = [_empty(nxt.total_dim) for _ in range(lvl.budget)]
+        keep += [rhs, ws, cos, ts]
+        n = len(ws)
+        arr_w = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in ws])
+        arr_c = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in cos])
+        _lib.check(lib.pmk_hier_set_buffers(H, idx, _lib.ptr(rhs), arr_w, arr_c, n,
+                                            _lib.ptr(ts)), "set_buffers")
+    crhs = _empty(hier.levels[-1].total_dim)
+    keep.append(crhs)
+    _lib.check(lib.pmk_hier_set_buffers(H, L - 1, _lib.ptr(crhs), None, None, 0, None),
+               "set_buffers")
+
+
+# --------------------------------------------------------------------- solve
+def apply_preconditioner(hier: LevelHierarchy, level_idx: int, v, ledger=None, model=None):
+    """v - Z A_H^{-1} Y^T (A v - mu v) at one level (reference solver.py:323-359)."""
+    if not 0 <= level_idx < hier.n_levels - 1:
+        raise ValueError("level_idx must index a non-coarsest level")
+    shape = tuple(v.shape) if hasattr(v, "shape") else np.shape(v)
+    dv, was_np = _to_device(v)
+    lvl, nxt = hier.levels[level_idx], hier.levels[level_idx + 1]
+    if dv.numel() != lvl.total_dim:
+        raise ValueError("vector size does not match the level")
+    out = _empty(lvl.total_dim)
+    child = _empty(nxt.total_dim)
+    lib = _lib.load()
+    _lib.check(lib.pmk_apply_preconditioner(hier._native, level_idx, _lib.ptr(dv),
+                                            _lib.ptr(child), _lib.ptr(out), _lib.stream_ptr()),
+               "apply_preconditioner")
+    return out.cpu().numpy().reshape(shape) if was_np else out.reshape(shape)
+
+
+def _state(hier, level_idx, want_arrays=False):
+    lib = _lib.load()
+    sc = (ctypes.c_double * 4)()
+    cap = ctypes.c_int32(0)
+    _lib.check(lib.pmk_fgmres_state(hier._native, level_idx, sc, None, None, None,
+                                    ctypes.byref(cap), _lib.stream_ptr()), "state")
+    out = {"beta": sc[0], "rel": sc[1], "n_iter": int(sc[2]), "breakdown": bool(sc[3]),
+           "cap": cap.value}
+    if want_arrays:
+        c = cap.value
+        hist = (ctypes.c_double * c)()
+        hraw = (ctypes.c_double * ((c + 1) * c))()
+        y = (ctypes.c_double * c)()
+        _lib.check(lib.pmk_fgmres_state(hier._native, level_idx, sc, hist, hraw, y, None,
+                                        _lib.stream_ptr()), "state")
+        out["hist"] = np.frombuffer(hist, dtype=np.float64).copy()
+        out["hraw"] = np.frombuffer(hraw, dtype=np.float64).copy().reshape(c + 1, c)
+        out["y"] = np.frombuffer(y, dtype=np.float64).copy()
+    return out
+
+
+def _check_memory(nbytes: int) -> None:
+    import torch
+
+    free, _total = torch.cuda.mem_get_info()
+    reserve = torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+    if nbytes > free + reserve - (256 << 20):
+        raise MemoryError(
+            f"FGMRES basis needs {nbytes / 2**30:.1f} GiB more device memory than is free; "
+            "set SolverConfig.restart to bound the basis")
+
+
+def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_iter: int,
+           ledger=None, model=None, keep_basis: bool = False):
+    """Right-preconditioned FGMRES, MGS + Givens, zero initial guess, no
+    restarts (reference solver.py:362-456).  tol=None runs exactly max_iter
+    iterations (inner solves) unless the basis breaks down."""
+    import torch
+
+    if not 0 <= level_idx < hier.n_levels - 1:
+        raise ValueError("fgmres runs on a non-coarsest level")
+    lib = _lib.load()
+    lvl, nxt = hier.levels[level_idx], hier.levels[level_idx + 1]
+    b, _ = _to_device(rhs)
+    b = b.reshape(-1)
+    if b.numel() != lvl.total_dim:
+        raise ValueError("rhs size does not match the level")
+    report = SolveReport(method=f"fgmres[level {level_idx}]",
+                         tol=tol if tol is not None else 0.0)
+    s = _lib.stream_ptr()
+    H = hier._native
+    _lib.check(lib.pmk_fgmres_begin(H, level_idx, _lib.ptr(b), int(max_iter),
+                                    float(tol) if tol is not None else 0.0, s), "fgmres_begin")
+    st = _state(hier, level_idx)
+    if st["beta"] == 0.0:
+        return torch.zeros_like(b), report
+    ws, cos = [], []
+    per_iter = 8 * (lvl.total_dim + nxt.total_dim)
+    for j in range(max_iter):
+        _check_memory(per_iter)
+        w = _empty(lvl.total_dim)
+        co = _empty(nxt.total_dim)
+        ws.append(w)
+        cos.append(co)
+        _lib.check(lib.pmk_fgmres_step(H, level_idx, j, _lib.ptr(w), _lib.ptr(co), s),
+                   "fgmres_step")
+        if tol is not None:
+            st = _state(hier, level_idx)
+            if st["breakdown"] or st["rel"] <= tol:
+                break
+    x = _empty(lvl.total_dim)
+    _lib.check(lib.pmk_fgmres_finish(H, level_idx, _lib.ptr(x), s), "fgmres_finish")
+    st = _state(hier, level_idx, want_arrays=True)
+    n_iter = st["n_iter"]
+    report.outer_iterations = n_iter
+    report.residual_history = [float(r) for r in st["hist"][:n_iter]]
+    if st["breakdown"] or (tol is not None and n_iter and report.residual_history[-1] <= tol):
+        report.converged = True
+    if keep_basis:
+        scales = [st["beta"]] + [st["hraw"][l, l - 1] for l in range(1, n_iter + 1)]
+        raws = [b] + ws
+        n_basis = n_iter if st["breakdown"] else n_iter + 1
+        basis = [(raws[l] / scales[l]).cpu().numpy() for l in range(n_basis)]
+        pre = []
+        for l in range(n_iter):
+            vl = raws[l] / scales[l]
+            t = lvl.pair.interpolate(cos[l])
+            pre.append((vl - t).cpu().numpy())
+        report.metadata["basis"] = basis
+        report.metadata["preconditioned"] = pre
+        report.metadata["hessenberg"] = st["hraw"][:n_iter + 1, :n_iter].copy()
+    del ws, cos
+    return x, report
+
+
+def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart: int):
+    """FGMRES(m): cycles of the reference fgmres on the current residual
+    (SURVEY.md section 8(c) restart oracle)."""
+    import torch
+
+    fine = hier.fine
+    b = fine.rhs.reshape(-1)
+    beta0 = _nrm2(b)
+    x = torch.zeros_like(b)
+    r = b.clone()
+    hist: list[float] = []
+    total = 0
+    cycles = 0
+    converged = False
+    while total < max_outer:
+        rn = _nrm2(r)
+        if rn == 0.0:
+            converged = True
+            break
+        m = min(restart, max_outer - total)
+        dx, rep = fgmres(hier, 0, r, tol=tol * beta0 / rn, max_iter=m)
+        x = x + dx
+        total += rep.outer_iterations
+        cycles += 1
+        hist += [h * rn / beta0 for h in rep.residual_history]
+        ax = torch.empty_like(b)
+        fine.matvec_into(x, ax)
+        r = b - ax
+        if _nrm2(r) / beta0 <= tol:
+            converged = True
+            break
+        if rep.outer_iterations == 0:
+            break
+    report = SolveReport(method="fgmres[level 0]", tol=tol)
+    report.outer_iterations = total
+    report.residual_history = hist
+    report.converged = converged
+    report.metadata["restart_cycles"] = cycles
+    return x, report
+
+
+def _nrm2(t) -> float:
+    import torch
+
+    lib = _lib.load()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+    _lib.check(lib.pmk_nrm2(_lib.ptr(t), t.numel(), _lib.ptr(out), _lib.stream_ptr()), "nrm2")
+    return float(out.item())
+
+
+def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | None = None):
+    import torch
+
+    cfg = hier.config
+    rhs = hier.fine.rhs.reshape(-1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if cfg.restart is None:
+        x, report = fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer)
+    else:
+        x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart)
+    torch.cuda.synchronize()
+    report.method = method_name
+    report.wall_time = time.perf_counter() - t0
+    report.tol = cfg.tol
+    true_res = hier.fine.relative_residual(x)
+    report.metadata["true_relative_residual"] = true_res
+    report.converged = true_res <= cfg.tol
+    report.level_stats = {"levels": hier.describe(), "moves": hier.moves}
+    if output is None:
+        output = "host" if hier.fine.host_io else "device"
+    if output == "host":
+        return x.cpu().numpy(), report
+    return x, report
+
+
+def two_level_solve(hier: LevelHierarchy, ledger=None, model=None, output: str | None = None):
+    if hier.n_levels != 2:
+        raise ValueError("two_level_solve expects a 2-level hierarchy")
+    return _solve(hier, ledger, model, "two_level", output)
+
+
+def multilevel_solve(hier: LevelHierarchy, ledger=None, model=None, output: str | None = None):
+    """Outer FGMRES to cfg.tol (reference solver.py:459-488).  Returns x as
+    numpy when the fine system was built from a numpy u0, else as a device
+    tensor (``output`` = "host" / "device" overrides)."""
+    return _solve(hier, ledger, model, f"multilevel[{hier.n_levels}]", output)

@@ -1,0 +1,173 @@
+"""Seeded workload definitions shared by the golden-fixture generator, the
+oracle tests, the GPU parity tests and bench.py.
+
+u0 recipes follow BASELINE.json:
+  * "bump":  initial_bump + 0.1 * N(0,1) noise, rng = default_rng(seed)
+  * "modes": sum of 8 sine modes, indices rng.integers(1, 17, (8, 2)) drawn
+             first, then amplitudes rng.standard_normal(8)
+The literal BASELINE configs run at Courant numbers 24-512, where the
+reference MLK stagnates; the "_c" companions keep
+the shapes and pick T so that C matches the paper (0.64 in 1-D, 0.16 in
+2-D), as SURVEY.md section 8(d) recommends.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Case:
+    name: str
+    dim: int
+    nx: int
+    n_t: int
+    theta: float
+    n_levels: int
+    schedule: tuple
+    nu: int = 2
+    T: float | None = None          # final time (dt = T / n_t) ...
+    courant: float | None = None    # ... or dt from the Courant number
+    u0: str = "bump"
+    seed: int = 0
+    mu: float = 1.0
+    tol: float = 1e-8
+    max_outer: int = 200
+    inner_iters: object = None
+    n_cgs: int = 0
+    restart: int | None = None
+    two_level_family: str | None = None   # use build_two_level(family) instead
+
+    @property
+    def ny(self) -> int:
+        return self.nx if self.dim == 2 else 1
+
+    @property
+    def m(self) -> int:
+        return self.nx * self.ny
+
+    @property
+    def N(self) -> int:
+        return (self.n_t + 1) * self.m
+
+    def dx(self) -> float:
+        return 1.0 / (self.nx + 1)
+
+    def dt(self) -> float:
+        if self.T is not None:
+            return self.T / self.n_t
+        factor = 2.0 if self.dim == 1 else 3.0
+        return self.courant * self.dx() ** 2 / factor
+
+    def u0_vector(self) -> np.ndarray:
+        rng = np.random.default_rng(self.seed)
+        nx, ny, h = self.nx, self.ny, self.dx()
+        x = np.arange(1, nx + 1) * h
+        if self.u0 == "bump":
+            gx = np.sin(np.pi * x / (h * (nx + 1)))
+            if self.dim == 1:
+                base = gx
+            else:
+                y = np.arange(1, ny + 1) * h
+                gy = np.sin(np.pi * y / (h * (ny + 1)))
+                base = np.outer(gy, gx).ravel()
+            return base + 0.1 * rng.standard_normal(self.m)
+        if self.u0 == "modes":
+            idx = rng.integers(1, 17, size=(8, 2))
+            amp = rng.standard_normal(8)
+            y = np.arange(1, ny + 1) * h
+            u = np.zeros((ny, nx))
+            for (p, q), a in zip(idx, amp):
+                if self.dim == 1:
+                    u[0] += a * np.sin(p * np.pi * x)
+                else:
+                    u += a * np.outer(np.sin(q * np.pi * y), np.sin(p * np.pi * x))
+            return u.ravel()
+        raise ValueError(self.u0)
+
+    def scaled(self, **kw) -> "Case":
+        d = dict(self.__dict__)
+        d.update(kw)
+        return Case(**d)
+
+
+# Small cases: the CPU oracle finishes each in well under a second.
+SMALL = {
+    # config-1 shape, shrunk: 1-D theta=1, 2-level T, exact coarsest
+    "c1_small": Case("c1_small", 1, 15, 32, 1.0, 2, ("time",), T=0.02),
+    # config-1 literal regime (C=32 at n=63): fixed budget, decoupled coarsest
+    "c1_lit_small": Case("c1_lit_small", 1, 15, 32, 1.0, 2, ("time",), T=1.0, n_cgs=4,
+                         max_outer=12),
+    # config-2 shape, shrunk: 1-D CN, 4 levels
+    "c2_small": Case("c2_small", 1, 31, 64, 0.5, 4, ("time",) * 3, courant=0.64),
+    # config-3 shape, shrunk: 2-D CN, 3 levels
+    "c3_small": Case("c3_small", 2, 7, 32, 0.5, 3, ("time",) * 2, courant=0.16),
+    # config-4 shape, shrunk: 2-D theta=1, TS x TS nu=4 (agglomeration), odd grid
+    "c4_small": Case("c4_small", 2, 15, 64, 1.0, 3, ("time_space",) * 2, nu=4, courant=0.16,
+                     u0="modes", max_outer=40),
+    # config-5 shape, shrunk: 2-D CN, 5 levels, perturbed decoupled coarsest
+    "c5_small": Case("c5_small", 2, 15, 64, 0.5, 5, ("time",) * 4, courant=0.16, n_cgs=4),
+    # same with the exact coarsest chain and FGMRES(restart)
+    "c5_small_restart": Case("c5_small_restart", 2, 15, 64, 0.5, 5, ("time",) * 4,
+                             courant=0.16, restart=4),
+    # [time, space] schedule (space move on an odd grid: transpose semantics)
+    "space_small": Case("space_small", 2, 15, 16, 1.0, 3, ("time", "space"), courant=0.16,
+                        max_outer=30),
+    # 2-level TS family (build_two_level)
+    "ts2_small": Case("ts2_small", 1, 31, 32, 0.5, 2, ("TS",), courant=0.64,
+                      two_level_family="TS", max_outer=40),
+}
+
+# BASELINE.json configs (literal) and their regime-adjusted companions.
+BASELINE = {
+    "c1": Case("c1", 1, 63, 256, 1.0, 2, ("time",), T=1.0, n_cgs=128),
+    "c2": Case("c2", 1, 1023, 4096, 0.5, 4, ("time",) * 3, T=1.0),
+    "c3": Case("c3", 2, 63, 512, 0.5, 3, ("time",) * 2, T=1.0),
+    "c4": Case("c4", 2, 127, 1024, 1.0, 3, ("time_space",) * 2, nu=4, T=1.0, u0="modes"),
+    "c5": Case("c5", 2, 255, 4096, 0.5, 5, ("time",) * 4, T=1.0, n_cgs=256, restart=30),
+    "c1_c": Case("c1_c", 1, 63, 256, 1.0, 2, ("time",), courant=0.64),
+    "c2_c": Case("c2_c", 1, 1023, 4096, 0.5, 4, ("time",) * 3, courant=0.64),
+    "c3_c": Case("c3_c", 2, 63, 512, 0.5, 3, ("time",) * 2, courant=0.16),
+    "c4_c": Case("c4_c", 2, 127, 1024, 1.0, 3, ("time_space",) * 2, nu=4, courant=0.16,
+                 u0="modes"),
+    # headline workload: config-5 shape at the paper's Courant number, exact
+    # coarsest chain (grid-independent ~19 iterations), FGMRES(30)
+    "c5_c": Case("c5_c", 2, 255, 4096, 0.5, 5, ("time",) * 4, courant=0.16, restart=30),
+    # decoupled variant (one independent solve per coarse slice)
+    "c5_c_dec": Case("c5_c_dec", 2, 255, 4096, 0.5, 5, ("time",) * 4, courant=0.16,
+                     n_cgs=256, restart=30),
+    # mid-size companions the CPU oracle solves in seconds
+    "mid_2d": Case("mid_2d", 2, 63, 256, 0.5, 5, ("time",) * 4, courant=0.16),
+}
+
+
+def oracle_hierarchy(case: Case):
+    """Build the CPU oracle hierarchy for a case (test infrastructure)."""
+    from oracle import pintmk_oracle as O
+
+    cfg = O.Config(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
+                   inner_iters=case.inner_iters, coarsest_n_cgs=case.n_cgs,
+                   restart=case.restart)
+    if case.two_level_family is not None:
+        fam = {"T": ["time"], "TS": ["time_space"]}[case.two_level_family]
+        return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
+                       case.u0_vector(), 2, fam, cfg, nu=case.nu)
+    return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
+                   case.u0_vector(), case.n_levels, list(case.schedule), cfg, nu=case.nu)
+
+
+def gpu_hierarchy(case: Case, u0=None):
+    """Build the device hierarchy through the product's public API."""
+    import paper_2401_00228_b200 as P
+
+    op = P.build_laplacian(case.dim, case.nx, case.ny if case.dim == 2 else 1)
+    ops = P.build_step_operators(op, P.ThetaSchemeConfig(case.theta, case.dt(), case.n_t))
+    fine = P.FineSystem(ops, case.u0_vector() if u0 is None else u0)
+    cfg = P.SolverConfig(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
+                         inner_iters=case.inner_iters, coarsest_n_cgs=case.n_cgs,
+                         restart=case.restart)
+    if case.two_level_family is not None:
+        return P.build_two_level(fine, case.two_level_family, case.nu, cfg)
+    return P.build_hierarchy(fine, case.n_levels, list(case.schedule), cfg, nu=case.nu)

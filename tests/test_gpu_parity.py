@@ -1,0 +1,169 @@
+"""GPU parity: the sm_100a path (through the public API / C-ABI) against the
+CPU oracle and the committed golden fixtures of the reference.
+
+Tolerances (fp64):
+  * matvec, restrict, interpolate: bitwise (same operations, same order);
+  * coarsest forward_solve: <= 1e-12 relative l2 (sine-diagonalised /
+    dense-inverse solve vs the reference's LU / Thomas: rounding only);
+  * apply_preconditioner (contains inner FGMRES + coarsest solve): <= 1e-10;
+  * full solve: same iteration count (+-1) and x within 1e-10 relative l2 of
+    the reference (the north-star parity bar).
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from tests.cases import SMALL, gpu_hierarchy, oracle_hierarchy
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def golden(name):
+    return np.load(os.path.join(GOLDEN, f"{name}.npz"))
+
+
+def rel(a, b):
+    a = np.asarray(a).ravel()
+    b = np.asarray(b).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_matvec_bitwise(name):
+    g = golden(name)
+    h = gpu_hierarchy(SMALL[name])
+    out = h.levels[0].system.matvec(g["mv_in"])
+    np.testing.assert_array_equal(out, g["mv_out"])
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_transfers_bitwise(name):
+    g = golden(name)
+    h = gpu_hierarchy(SMALL[name])
+    for i, lv in enumerate(h.levels[:-1]):
+        np.testing.assert_array_equal(lv.pair.restrict(g[f"r{i}_in"]), g[f"r{i}_out"])
+        np.testing.assert_array_equal(lv.pair.interpolate(g[f"i{i}_in"]), g[f"i{i}_out"])
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_coarsest_forward_solve(name):
+    g = golden(name)
+    h = gpu_hierarchy(SMALL[name])
+    out = h.levels[-1].system.forward_solve(g["cs_in"])
+    assert rel(out, g["cs_out"]) <= 1e-12
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_apply_preconditioner(name):
+    from paper_2401_00228_b200 import apply_preconditioner
+
+    g = golden(name)
+    h = gpu_hierarchy(SMALL[name])
+    out = apply_preconditioner(h, 0, g["pc_in"])
+    assert rel(out, g["pc_out"]) <= 1e-10
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_solve_parity(name):
+    from paper_2401_00228_b200 import multilevel_solve
+
+    case = SMALL[name]
+    g = golden(name)
+    h = gpu_hierarchy(case)
+    x, rep = multilevel_solve(h)
+    assert abs(rep.outer_iterations - int(g["iters"])) <= 1
+    assert rel(x, g["x"]) <= 1e-10, rel(x, g["x"])
+    hist = np.array(rep.residual_history)
+    k = min(len(hist), len(g["hist"]))
+    assert np.allclose(hist[:k], g["hist"][:k], rtol=1e-6, atol=1e-14)
+
+
+@pytest.mark.parametrize("name", ["c3_small", "c5_small"])
+def test_fgmres_internals_vs_oracle(name):
+    """Basis, preconditioned vectors and Hessenberg of a 3-iteration solve."""
+    from oracle import pintmk_oracle as O
+    from paper_2401_00228_b200 import fgmres
+
+    case = SMALL[name]
+    h = gpu_hierarchy(case)
+    oh = oracle_hierarchy(case)
+    rhs = oh.rhs.ravel()
+    x, rep = fgmres(h, 0, rhs, tol=None, max_iter=3, keep_basis=True)
+    xo, info = O.fgmres(oh, 0, rhs, None, 3, keep_basis=True)
+    assert rep.outer_iterations == info["iterations"] == 3
+    for a, b in zip(rep.metadata["basis"], info["basis"]):
+        assert rel(a, b) <= 1e-11
+    for a, b in zip(rep.metadata["preconditioned"], info["preconditioned"]):
+        assert rel(a, b) <= 1e-11
+    np.testing.assert_allclose(rep.metadata["hessenberg"], info["hessenberg"], rtol=1e-10,
+                               atol=1e-13)
+    assert rel(x.cpu().numpy(), xo) <= 1e-10
+
+
+def test_solve_is_deterministic():
+    from paper_2401_00228_b200 import multilevel_solve
+
+    case = SMALL["c5_small"]
+    x1, r1 = multilevel_solve(gpu_hierarchy(case))
+    x2, r2 = multilevel_solve(gpu_hierarchy(case))
+    np.testing.assert_array_equal(x1, x2)
+    assert r1.residual_history == r2.residual_history
+
+
+def test_device_io_roundtrip():
+    """A device-resident u0 gives a device x equal to the host path's."""
+    import torch
+
+    from paper_2401_00228_b200 import multilevel_solve
+
+    case = SMALL["c3_small"]
+    xh, _ = multilevel_solve(gpu_hierarchy(case))
+    xd, _ = multilevel_solve(gpu_hierarchy(case, u0=torch.from_numpy(case.u0_vector()).cuda()))
+    assert isinstance(xd, torch.Tensor) and xd.is_cuda
+    np.testing.assert_array_equal(xd.cpu().numpy(), xh)
+
+
+def test_sequential_solve_matches_oracle():
+    from oracle import pintmk_oracle as O
+    from paper_2401_00228_b200 import (ThetaSchemeConfig, build_laplacian,
+                                       build_step_operators, sequential_solve)
+
+    case = SMALL["c3_small"]
+    op = build_laplacian(2, case.nx, case.nx)
+    ops = build_step_operators(op, ThetaSchemeConfig(case.theta, case.dt(), case.n_t))
+    u0 = case.u0_vector()
+    out = sequential_solve(ops, u0)
+    a, _ = O.laplacian(2, case.nx, case.nx)
+    d, b = O.blocks_from(a, case.theta, case.dt())
+    ref = O.sequential(d, b, u0, case.n_t)
+    assert rel(out, ref) <= 1e-12
+
+
+def test_zero_rhs_returns_zero():
+    from paper_2401_00228_b200 import fgmres
+
+    h = gpu_hierarchy(SMALL["c3_small"])
+    x, rep = fgmres(h, 0, np.zeros(h.levels[0].total_dim), tol=1e-8, max_iter=5)
+    assert float(abs(x).max()) == 0.0 and rep.outer_iterations == 0
+
+
+def test_bad_shapes_raise():
+    import paper_2401_00228_b200 as P
+
+    h = gpu_hierarchy(SMALL["c3_small"])
+    with pytest.raises(ValueError):
+        h.levels[0].system.matvec(np.zeros(7))
+    with pytest.raises(ValueError):
+        P.apply_preconditioner(h, 2, np.zeros(h.levels[2].total_dim))
