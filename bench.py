@@ -1,0 +1,318 @@
+#!/usr/bin/env python
+"""Benchmark: all-at-once space-time MLK solve on B200.
+
+Metric (BASELINE.json): space-time unknowns/s to a 1e-8 relative residual.
+A "step" is one complete multilevel_solve (outer FGMRES to tol, inner
+recursion, coarsest solves, true-residual check) of the workload.
+
+Default workload ("c5_c"): the BASELINE config-5 shape -- 2-D heat equation,
+255x255 interior grid, n_t = 4096 (2.66e8 unknowns, 2.13 GB per vector),
+theta = 1/2, 5-level MLK, nu = 2, FGMRES(30), tol 1e-8 -- at the paper's
+Courant number C = 0.16 (the literal T = 1 gives C = 48, where the reference
+MLK stagnates; SURVEY.md sections 0.3 and 8(d)).  Seeded synthetic u0
+(sin(pi x) sin(pi y) + 0.1 N(0,1)).  Every vector is larger than L2, so no
+L2 flush is needed between steps.
+
+  value  device-resident: u0 and the hierarchy already on the GPU, CUDA
+         events around K solves, max over ranks.
+  e2e    through the public API with host buffers: pinned u0 -> FineSystem
+         -> build_hierarchy -> multilevel_solve -> x into pinned host memory.
+  --gpus N > 1 (torchrun): every rank solves its own seeded instance
+         (independent problems, no data-path collective): weak scaling.
+  --impl reference: the CPU oracle (numpy/scipy restatement of pintmk,
+         bitwise equal to the reference) on the host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time unknowns/s to 1e-8 rel. residual"
+UNIT = "unknowns/s"
+CPU_SAMPLE = "mid_2d"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--case", default="c5_c")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    return ap.parse_args()
+
+
+def dist_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cpu_sample_solve():
+    """One CPU-oracle solve of the bounded sample; returns (unknowns/s, seconds, info)."""
+    from oracle import pintmk_oracle as O
+    from tests.cases import BASELINE, oracle_hierarchy
+
+    case = BASELINE[CPU_SAMPLE]
+    h = oracle_hierarchy(case)
+    t0 = time.perf_counter()
+    x, info = O.solve(h)
+    dt = time.perf_counter() - t0
+    return case.N / dt, dt, info, case
+
+
+def cpu_desc(case, info):
+    return (f"CPU oracle (numpy/scipy restatement of pintmk, bitwise equal to the reference) "
+            f"full solve of the {case.nx}x{case.nx} x {case.n_t}-step companion of the workload "
+            f"(same theta, levels, nu, Courant number; {info['iterations']} iterations, "
+            f"{case.N} unknowns); scipy sparse/SuperLU single-threaded, BLAS-1 dots on "
+            f"OpenBLAS default threads")
+
+
+def run_reference(args):
+    rank, world, _ = dist_info()
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(min(args.warmup, 1)):
+        cpu_sample_solve()
+    for _ in range(args.steps):
+        v, dt, info, case = cpu_sample_solve()
+        vals.append(v)
+    value = statistics.mean(vals)
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "ms_per_step": 1000.0 * case.N / value, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.case, "sample": CPU_SAMPLE},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": cpu_desc(case, info)},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2401_00228_b200 import _lib, multilevel_solve
+    from tests.cases import BASELINE, gpu_hierarchy
+
+    rank, world, local = dist_info()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    case = BASELINE[args.case].scaled(seed=BASELINE[args.case].seed + rank)
+    u0 = torch.from_numpy(case.u0_vector()).cuda()
+    hier = gpu_hierarchy(case, u0=u0)
+
+    for _ in range(max(args.warmup, 0)):
+        x, rep = multilevel_solve(hier)
+        del x
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    profile = not args.no_profile
+    if profile:
+        _lib.profile_begin(True)
+    n0 = _lib.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    iters, trues = [], []
+    ev0.record()
+    for _ in range(args.steps):
+        x, rep = multilevel_solve(hier)
+        iters.append(rep.outer_iterations)
+        trues.append(rep.metadata["true_relative_residual"])
+        del x
+    ev1.record()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - n0
+    kernels = _lib.profile_end() if profile else {}
+    clocks = sampler.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    ms_per_step = ms / args.steps
+    value = case.N * args.steps * world / (ms / 1000.0)
+
+    # ----- e2e: public API, host buffers, H2D + setup + solve + D2H per step
+    pin_u0 = torch.from_numpy(case.u0_vector()).pin_memory()
+    pin_x = torch.empty(case.N, dtype=torch.float64).pin_memory()
+    del hier
+    torch.cuda.empty_cache()
+    e2e_t = []
+    for _ in range(max(args.e2e_steps, 0)):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        h2 = gpu_hierarchy(case, u0=pin_u0)
+        xh, rep2 = multilevel_solve(h2, out=pin_x)
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+        del h2, xh
+        torch.cuda.empty_cache()
+    e2e_s = max(e2e_t) if e2e_t else float("nan")
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    # ----- roofline of the dominant memory-bound kernel
+    peak, peak_kind = peaks()
+    roof = None
+    table = {}
+    for name, k in kernels.items():
+        gbs = k["bytes"] / (k["ms"] / 1000.0) / 1e9 if k["ms"] > 0 else 0.0
+        table[name] = {"launches": k["launches"], "ms": round(k["ms"], 3),
+                       "share": round(k["ms"] / ms, 4) if ms else None,
+                       "GB/s": round(gbs, 1),
+                       "TFLOP/s": round(k["flops"] / (k["ms"] / 1000.0) / 1e12, 2)
+                       if k["ms"] > 0 and k["flops"] else None}
+    mem = {n: k for n, k in kernels.items() if n not in ("coarse_gemm", "fgmres_small")}
+    if mem:
+        dom = max(mem, key=lambda n: mem[n]["ms"])
+        k = mem[dom]
+        achieved = k["bytes"] / (k["ms"] / 1000.0) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get(dom)
+            except Exception:
+                traffic = None
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1),
+                "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                "traffic": traffic, "bytes_per_launch": k["bytes"] / k["launches"],
+                "peak_source": peak_kind}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, info, c = cpu_sample_solve()
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+               "sample": cpu_desc(c, info) + f"; {dt:.1f} s"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded u0 = sin(pi x) sin(pi y) + 0.1 N(0,1); no dataset)",
+            "config": {"workload": case.name, "grid": f"{case.nx}x{case.ny}", "n_t": case.n_t,
+                       "theta": case.theta, "levels": case.n_levels, "nu": case.nu,
+                       "schedule": list(case.schedule), "courant": case.courant,
+                       "coarsest_n_cgs": case.n_cgs, "restart": case.restart, "tol": case.tol,
+                       "unknowns": case.N, "per_rank_instances": 1,
+                       "l2": "inputs larger than L2 (2.13 GB vectors), no flush needed"},
+            "iterations": iters[-1] if iters else None,
+            "true_relative_residual": max(trues) if trues else None,
+            "e2e": None if not e2e_t else {"value": case.N * world / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * case.m, "d2h_bytes_per_step": 8 * case.N,
+                    "seconds_per_step": e2e_s,
+                    "includes": "H2D of u0 from pinned memory, hierarchy setup, solve, "
+                                "D2H of x into pinned memory"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks,
+            "kernels": table,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

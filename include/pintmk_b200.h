@@ -182,25 +182,28 @@ int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C);
 
 /* Buffers of an inner level (1 <= idx < n_levels-1), or of the coarsest
  * (idx = n_levels-1: rhs only).  rhs receives the parent's restriction;
- * w_slots[budget] hold the unnormalised Krylov vectors; child_out[budget]
+ * v_slots[budget] receive the normalised Krylov vectors v_0..v_{budget-1};
+ * w_buf holds the unnormalised new vector of each iteration; child_out[budget]
  * (size of level idx+1) receive the child solve of each iteration;
  * ts_scratch ((n_T+1)*m_fine doubles) is required for space pairs. */
 int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs,
-                         double *const *w_slots, double *const *child_out,
-                         int32_t n_slots, double *ts_scratch);
+                         double *const *v_slots, double *const *child_out,
+                         int32_t n_slots, double *w_buf, double *ts_scratch);
 
 /* fgmres (solver.py:362-456) driven one iteration at a time.
- * begin: beta = ||rhs||, basis[0] = rhs / beta (lazily).  step j: one
- * iteration (preconditioner solver.py:323-359, matvec, MGS, Givens), writing
- * the unnormalised next basis vector into w_next and the child solve into
+ * begin: beta = ||rhs||.  step j: one iteration (preconditioner
+ * solver.py:323-359, matvec, MGS, Givens): its first pass stores the
+ * normalised basis vector v_j into v_out (rhs/beta for j = 0, else the
+ * previous step's w / h[j][j-1]); the unnormalised next vector goes to w_next
+ * (may be the previous step's w_next, never the rhs) and the child solve to
  * child_out.  tol > 0 stops the device-side iteration once rel <= tol
  * (solver.py:438); tol = 0 is the reference's tol=None.  finish: back substitution
  * and x = sum_i y_i x_i with x_i = v_i - Z vt_i recomputed (no stored
  * preconditioned vectors). */
 int pmk_fgmres_begin(pmk_hier *H, int32_t idx, const double *rhs,
                      int32_t max_iter, double tol, pmk_stream_t stream);
-int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *w_next,
-                    double *child_out, pmk_stream_t stream);
+int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *v_out,
+                    double *w_next, double *child_out, pmk_stream_t stream);
 int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x,
                       pmk_stream_t stream);
 /* Copies the level's fgmres state to the host (synchronises the stream):

@@ -70,9 +70,10 @@ SIGNATURES = {
                                      POINTER(PairDesc), c_int32]),
     "pmk_hier_set_coarse": (c_int32, [c_void_p, POINTER(CoarseDesc)]),
     "pmk_hier_set_buffers": (c_int32, [c_void_p, c_int32, c_void_p, POINTER(c_void_p),
-                                       POINTER(c_void_p), c_int32, c_void_p]),
+                                       POINTER(c_void_p), c_int32, c_void_p, c_void_p]),
     "pmk_fgmres_begin": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_double, c_void_p]),
-    "pmk_fgmres_step": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p]),
+    "pmk_fgmres_step": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
     "pmk_fgmres_finish": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
     "pmk_fgmres_state": (c_int32, [c_void_p, c_int32, POINTER(c_double), POINTER(c_double),
                                    POINTER(c_double), POINTER(c_double), POINTER(c_int32),
@@ -80,6 +81,10 @@ SIGNATURES = {
     "pmk_fgmres_fixed": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
     "pmk_apply_preconditioner": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p,
                                            c_void_p]),
+    "pmk_profile_begin": (c_int32, [c_int32]),
+    "pmk_profile_end": (c_int32, [POINTER(c_double), c_int32, POINTER(c_int32)]),
+    "pmk_profile_category": (ctypes.c_char_p, [c_int32]),
+    "pmk_launch_count": (c_int64, []),
 }
 
 _lib = None
@@ -143,6 +148,29 @@ def stream_ptr():
     import torch
 
     return c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def profile_begin(with_events: bool = True) -> None:
+    check(load().pmk_profile_begin(1 if with_events else 0), "profile_begin")
+
+
+def profile_end() -> dict:
+    """{category: {launches, ms, bytes, flops}} since profile_begin (synchronises)."""
+    lib = load()
+    stats = (c_double * 64)()
+    n = c_int32(0)
+    check(lib.pmk_profile_end(stats, 16, ctypes.byref(n)), "profile_end")
+    out = {}
+    for c in range(n.value):
+        name = lib.pmk_profile_category(c).decode()
+        launches, ms, nbytes, flops = stats[4 * c: 4 * c + 4]
+        if launches:
+            out[name] = {"launches": int(launches), "ms": ms, "bytes": nbytes, "flops": flops}
+    return out
+
+
+def launch_count() -> int:
+    return int(load().pmk_launch_count())
 
 
 def ptr(t) -> c_void_p:

@@ -4,10 +4,11 @@
 // The recursion mirrors reference solver.py:323-456 step for step:
 //
 //   fgmres(level, rhs, tol, max_iter)          solver.py:362-456
-//     beta = ||rhs||; v_0 = rhs / beta         (begin_kernel; v_0 kept lazy)
+//     beta = ||rhs||                            (begin_kernel)
 //     for j:
 //       x_j = apply_preconditioner(v_j)        solver.py:323-359
-//          vh = Y^T (A v_j - mu v_j)           K-MVR (one pass)
+//          vh = Y^T (A v_j - mu v_j)           K-MVR (one pass; also stores
+//                                              v_j = raw_j / h[j][j-1] or rhs / beta)
 //          vt = coarsest forward_solve(vh)     or fgmres(level+1, vh, None, budget)
 //          x_j = v_j - Z vt                    fused into K-IMV below
 //       w = A x_j                              K-IMV (+ partial <w, v_0>)
@@ -88,7 +89,8 @@ struct LevelRT {
   int64_t N = 0;
   // registered buffers (inner levels / coarsest rhs)
   double *rhs = nullptr;
-  std::vector<double *> w_slots, child_out;
+  std::vector<double *> v_slots, child_out;
+  double *w_buf = nullptr;
   double *ts_scratch = nullptr;
   // device state
   KState *d_state = nullptr;  // header in device memory
@@ -98,7 +100,9 @@ struct LevelRT {
   double *partA = nullptr, *partB = nullptr;
   double tol = 0.0;
   // current invocation
-  std::vector<const double *> vraw;  // raw basis vectors, index l
+  const double *rhs_cur = nullptr;   // rhs of this invocation (raw basis vector 0)
+  const double *pending = nullptr;   // unnormalised basis vector j (w of iteration j-1)
+  std::vector<const double *> v;     // normalised basis vectors, index l
   std::vector<const double *> vt;    // child outputs, iteration j
   const int *parent_live = nullptr;
 };
@@ -159,12 +163,14 @@ MarchParams base_params(const pmk_level &L) {
   return p;
 }
 
-// vh = Y^T (A v - mu v)
+// vh = Y^T (A v - mu v) ; optionally v_norm_out = v (normalised input)
 int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
-           const double *v_scale, double *vh, double *scratch, const int *live, cudaStream_t s) {
+           const double *v_scale, double *vh, double *scratch, double *v_norm_out,
+           const int *live, cudaStream_t s) {
   MarchParams p = base_params(L);
   p.v = v;
   p.v_scale = v_scale;
+  p.v_norm_out = v_norm_out;
   p.mu = mu;
   p.nu = P.nu;
   const bool space = P.group_of != nullptr;
@@ -253,7 +259,9 @@ int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double t
   if (rc) return rc;
   rc = launch_begin(R.d_state, R.partA, kRedBlocks, parent_live, s);
   if (rc) return rc;
-  R.vraw.assign(1, rhs);
+  R.rhs_cur = rhs;
+  R.pending = rhs;
+  R.v.clear();
   R.vt.clear();
   return 0;
 }
@@ -276,34 +284,36 @@ double *child_rhs(pmk_hier *H, int idx) {
   return H->lv[child].rhs;
 }
 
-int fgmres_step(pmk_hier *H, int idx, int j, double *w_next, double *child_out, cudaStream_t s) {
+int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
+                cudaStream_t s) {
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
   PMK_RETURN_IF(j != (int)R.vt.size() || j >= R.cap, PMK_ERR_STATE);
-  PMK_RETURN_IF(!w_next || !child_out, PMK_ERR_ARG);
+  PMK_RETURN_IF(!v_out || !w_next || !child_out, PMK_ERR_ARG);
+  PMK_RETURN_IF(w_next == R.rhs_cur || v_out == R.pending, PMK_ERR_ARG);
   double *vh = child_rhs(H, idx);
   PMK_RETURN_IF(!vh, PMK_ERR_STATE);
   const int *live = live_ptr(R);
   const KState &K = R.h_state;
-  const double *vj = R.vraw[j];
-  const double *sj = K.vscale + j;
-  // apply_preconditioner (solver.py:336-359)
-  int rc = do_mvr(R.L, R.P, H->mu, vj, sj, vh, R.ts_scratch, live, s);
+  // apply_preconditioner (solver.py:336-359); the pass that reads the
+  // unnormalised basis vector also stores v_j = raw / scale.
+  int rc = do_mvr(R.L, R.P, H->mu, R.pending, K.vscale + j, vh, R.ts_scratch, v_out, live, s);
   if (rc) return rc;
+  R.v.push_back(v_out);
   rc = child_solve(H, idx, child_out, live, s);
   if (rc) return rc;
   // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407)
   int np = 0;
-  rc = do_imv(R.L, R.P, vj, sj, child_out, nullptr, w_next, R.vraw[0], K.vscale, R.partA, &np,
-              live, s);
+  rc = do_imv(R.L, R.P, v_out, nullptr, child_out, nullptr, w_next, R.v[0], nullptr, R.partA,
+              &np, live, s);
   if (rc) return rc;
   // MGS (solver.py:405-408), then ||w|| on the last pass (solver.py:412)
   double *prev = R.partA, *cur = R.partB;
   int n_prev = np;
   for (int l = 0; l <= j; ++l) {
-    const double *vn = (l < j) ? R.vraw[l + 1] : nullptr;
-    rc = launch_mgs_pass(R.d_state, R.cap, l, j, w_next, R.vraw[l], K.vscale + l, vn,
-                         K.vscale + l + 1, R.N, prev, n_prev, cur, s);
+    const double *vn = (l < j) ? R.v[l + 1] : nullptr;
+    rc = launch_mgs_pass(R.d_state, R.cap, l, j, w_next, R.v[l], nullptr, vn, nullptr, R.N, prev,
+                         n_prev, cur, s);
     if (rc) return rc;
     double *t = prev;
     prev = cur;
@@ -312,7 +322,7 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *w_next, double *child_out, 
   }
   rc = launch_finish_col(R.d_state, R.cap, j, prev, n_prev, R.tol, s);
   if (rc) return rc;
-  R.vraw.push_back(w_next);
+  R.pending = w_next;
   R.vt.push_back(child_out);
   return 0;
 }
@@ -331,7 +341,7 @@ int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
     std::memset(&a, 0, sizeof(a));
     a.count = 0;
     for (int l = first; l < n && a.count < kAsmChunk; ++l) {
-      a.vraw[a.count] = R.vraw[l];
+      a.v[a.count] = R.v[l];
       a.vt[a.count] = R.vt[l];
       ++a.count;
     }
@@ -345,12 +355,13 @@ int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
 int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s) {
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.rhs, PMK_ERR_STATE);
-  PMK_RETURN_IF((int)R.w_slots.size() < R.budget || (int)R.child_out.size() < R.budget,
+  PMK_RETURN_IF((int)R.v_slots.size() < R.budget || (int)R.child_out.size() < R.budget ||
+                    !R.w_buf,
                 PMK_ERR_STATE);
   int rc = fgmres_begin(H, idx, R.rhs, R.budget, 0.0, parent_live, s);
   if (rc) return rc;
   for (int j = 0; j < R.budget; ++j) {
-    rc = fgmres_step(H, idx, j, R.w_slots[j], R.child_out[j], s);
+    rc = fgmres_step(H, idx, j, R.v_slots[j], R.w_buf, R.child_out[j], s);
     if (rc) return rc;
   }
   return fgmres_finish(H, idx, x, s);
@@ -446,7 +457,7 @@ int pmk_stmv_shift_restrict(const pmk_level *L, const pmk_pair *P, double mu,
   rc = check_pair(*L, P);
   if (rc) return rc;
   PMK_RETURN_IF(!v_raw || !vh, PMK_ERR_ARG);
-  return do_mvr(*L, *P, mu, v_raw, v_scale, vh, scratch, nullptr, cs(stream));
+  return do_mvr(*L, *P, mu, v_raw, v_scale, vh, scratch, nullptr, nullptr, cs(stream));
 }
 
 int pmk_interp_sub_stmv(const pmk_level *L, const pmk_pair *P, const double *v_raw,
@@ -542,8 +553,9 @@ int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C) {
   return 0;
 }
 
-int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *w_slots,
-                         double *const *child_out, int32_t n_slots, double *ts_scratch) {
+int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *v_slots,
+                         double *const *child_out, int32_t n_slots, double *w_buf,
+                         double *ts_scratch) {
   PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels || !rhs, PMK_ERR_ARG);
   if (idx == H->n_levels - 1) {
     H->coarse_rhs = rhs;
@@ -551,10 +563,12 @@ int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *w
   }
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
-  PMK_RETURN_IF(n_slots < 0 || (n_slots > 0 && (!w_slots || !child_out)), PMK_ERR_ARG);
+  PMK_RETURN_IF(n_slots < 0 || (n_slots > 0 && (!v_slots || !child_out || !w_buf)),
+                PMK_ERR_ARG);
   PMK_RETURN_IF(R.P.group_of && !ts_scratch, PMK_ERR_ARG);
   R.rhs = rhs;
-  R.w_slots.assign(w_slots, w_slots + n_slots);
+  R.w_buf = w_buf;
+  R.v_slots.assign(v_slots, v_slots + n_slots);
   R.child_out.assign(child_out, child_out + n_slots);
   R.ts_scratch = ts_scratch;
   return 0;
@@ -566,10 +580,10 @@ int pmk_fgmres_begin(pmk_hier *H, int32_t idx, const double *rhs, int32_t max_it
   return fgmres_begin(H, idx, rhs, max_iter, tol, nullptr, cs(stream));
 }
 
-int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *w_next, double *child_out,
-                    pmk_stream_t stream) {
+int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *v_out, double *w_next,
+                    double *child_out, pmk_stream_t stream) {
   PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
-  return fgmres_step(H, idx, j, w_next, child_out, cs(stream));
+  return fgmres_step(H, idx, j, v_out, w_next, child_out, cs(stream));
 }
 
 int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x, pmk_stream_t stream) {
@@ -618,7 +632,7 @@ int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v, double *
   cudaStream_t s = cs(stream);
   double *vh = child_rhs(H, idx);
   PMK_RETURN_IF(!vh, PMK_ERR_STATE);
-  int rc = do_mvr(R.L, R.P, H->mu, v, nullptr, vh, R.ts_scratch, nullptr, s);
+  int rc = do_mvr(R.L, R.P, H->mu, v, nullptr, vh, R.ts_scratch, nullptr, nullptr, s);
   if (rc) return rc;
   rc = child_solve(H, idx, child_out, nullptr, s);
   if (rc) return rc;

@@ -106,6 +106,9 @@ __global__ void __launch_bounds__(256)
 int gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B, int ldb,
          int64_t sB, double *C, int ldc, int64_t sC, int batch, const int *live, cudaStream_t s) {
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  const double flops = 2.0 * M * N * (double)K * batch;
+  const double bytes = 8.0 * batch * ((double)M * N * 2.0) + 8.0 * (double)K * N;
+  prof::Scope scope(prof::kGemm, bytes, flops, s);
   dgemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, live);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -121,7 +124,9 @@ __global__ void __launch_bounds__(256)
   if (!is_live(live)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
-  const double d = delta[i], b = beta[i];
+  // multiply by 1/delta: high modes decay through the subnormal range, where
+  // an IEEE division takes the slow path
+  const double d = 1.0 / delta[i], b = beta[i];
   double u = X[i];  // transformed rhs_0 == transformed out_0
   for (int k0 = 1; k0 <= n_steps; k0 += kRecBatch) {
     double r[kRecBatch];
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(256)
       const int k = k0 + q;
       if (k > n_steps) break;
       const bool cut = dropped && dropped[k];
-      u = cut ? r[q] / d : (r[q] + b * u) / d;
+      u = cut ? r[q] * d : fma(b, u, r[q]) * d;
       X[(int64_t)k * m + i] = u;
     }
   }
@@ -206,12 +211,12 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
   const int m = nx * ny;
   const int rows = C.n_steps + 1;
   const int64_t N = (int64_t)rows * m;
-  (void)N;
   if (C.kind == PMK_COARSE_DST) {
     PMK_RETURN_IF(!C.sx || !C.delta || !C.beta || !C.work0, PMK_ERR_ARG);
     if (ny == 1) {
       int rc = gemm(rows, nx, nx, rhs, nx, 0, C.sx, nx, 0, C.work0, nx, 0, 1, live, s);
       if (rc) return rc;
+      prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
       dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta, C.dropped,
                                                            C.n_steps, m, live);
       PMK_LAUNCH_CHECK();
@@ -225,6 +230,7 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       // S_y X_k per slice
       rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work0, nx, m, C.work1, nx, m, rows, live, s);
       if (rc) return rc;
+      prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
       dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta, C.dropped,
                                                            C.n_steps, m, live);
       PMK_LAUNCH_CHECK();
@@ -234,20 +240,28 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       if (rc) return rc;
     }
     // out_0 = rhs_0 exactly (stepper.py:118)
-    copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);
+    {
+      prof::Scope cs(prof::kCoarseMisc, 16.0 * m, 0.0, s);
+      copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);
+    }
     PMK_LAUNCH_CHECK();
     return 0;
   }
   if (C.kind == PMK_COARSE_DENSE) {
     PMK_RETURN_IF(!C.dinv || !C.work0, PMK_ERR_ARG);
-    copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);
+    {
+      prof::Scope cs(prof::kCoarseMisc, 16.0 * m, 0.0, s);
+      copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);
+    }
     PMK_LAUNCH_CHECK();
     const int cb = (m + 255) / 256 < 4 * kSMs ? (m + 255) / 256 : 4 * kSMs;
     const int gb = (m * 32 + 255) / 256;
     for (int k = 1; k <= C.n_steps; ++k) {
+      prof::Scope c1(prof::kCoarseMisc, 32.0 * m, 0.0, s);
       coupling_kernel<<<cb, 256, 0, s>>>(rhs + (int64_t)k * m, out + (int64_t)(k - 1) * m,
                                          C.work0, C.coupling, nx, ny, C.dropped, k, live);
       PMK_LAUNCH_CHECK();
+      prof::Scope c2(prof::kCoarseMisc, 8.0 * m * (double)m + 16.0 * m, 2.0 * m * (double)m, s);
       gemv_kernel<<<gb, 256, 0, s>>>(C.dinv, C.work0, out + (int64_t)k * m, m, live);
       PMK_LAUNCH_CHECK();
     }

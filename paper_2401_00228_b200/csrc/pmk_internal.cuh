@@ -130,7 +130,8 @@ struct MarchParams {
   // MVR
   double mu;
   int nu;
-  double *vh;  // (n_T+1, m) time-summed (fine spatial)
+  double *vh;          // (n_T+1, m) time-summed (fine spatial)
+  double *v_norm_out;  // optional: the normalised input v = v_raw / scale
   // IMV
   const double *vt;
   const int32_t *group_of;
@@ -145,6 +146,10 @@ struct MarchParams {
 // Launch one fused march.  Returns the number of partials written (IMV) via
 // *n_partials when non-null.
 int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials);
+// TMA-pipelined variant (pmk_march_tma.cu); *handled = 0 asks for the
+// register fallback.
+int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_partials,
+                     double bytes, int cat, int *handled);
 
 // ---------------------------------------------------------------- krylov
 int launch_dot_partials(const double *a, const double *a_scale, const double *b,

@@ -2,11 +2,12 @@
 // solver.py:362-456) and the stand-alone intergrid transfers
 // (intergrid.py:51-63, 106-120).
 //
-// Krylov basis vectors are stored UNNORMALISED: the reference appends
-// b / beta and w / h[j+1, j] (solver.py:395, 420); here the raw vector and
-// its divisor stay separate and every reader computes raw[i] / scale with an
-// IEEE division, which yields bitwise the values the reference stores while
-// saving a full read+write pass per iteration.
+// Krylov basis vectors: the reference appends b / beta and w / h[j+1, j]
+// (solver.py:395, 420).  Here the last MGS pass leaves w unnormalised and the
+// next iteration's K-MVR pass -- which reads it anyway -- divides by the norm
+// (IEEE division, bitwise the reference's values) and writes the normalised
+// v_j as a by-product (+8 B/unknown instead of a separate 16 B scale pass).
+// Every other reader (K-IMV, MGS, assembly) reads v_j division-free.
 //
 // All reductions are two-level with a fixed grid (kRedBlocks) and a fixed
 // summation order, so results are bitwise reproducible.  The second level is
@@ -88,6 +89,71 @@ __global__ void begin_kernel(KState *st, const double *partials, int n_partials,
 //   h[l][j] = <w, v_l>            (from the previous pass' partials)
 //   w      -= h[l][j] * v_l
 //   partial <w, v_{l+1}>          (or <w, w> on the last pass, solver.py:412)
+// Streams w, v_l, v_{l+1} as 16-byte vectors, two vectors per thread per
+// trip with all six loads issued before any use (memory-level parallelism:
+// 96 B in flight per thread).  Requires 16-byte aligned w / v_l / v_{l+1}
+// (checked on the host; the scalar variant below handles the rest).
+__global__ void __launch_bounds__(kRedThreads)
+    mgs_pass_vec_kernel(KState *st, int ld, int l, int j, double *__restrict__ w,
+                        const double *__restrict__ vl, const double *__restrict__ vn, int64_t n,
+                        const double *prev, int n_prev, double *partials) {
+  if (!st->live) return;
+  const double h = reduce_partials(prev, n_prev);
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->h[l * ld + j] = h;
+  const bool last = (vn == nullptr);
+  const int64_t n2 = n >> 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double2 *w2 = reinterpret_cast<double2 *>(w);
+  const double2 *l2 = reinterpret_cast<const double2 *>(vl);
+  const double2 *z2 = reinterpret_cast<const double2 *>(last ? w : vn);
+  double acc = 0.0;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; i + stride < n2; i += 2 * stride) {
+    const double2 a0 = w2[i], a1 = w2[i + stride];
+    const double2 b0 = __ldg(l2 + i), b1 = __ldg(l2 + i + stride);
+    double2 c0, c1;
+    if (!last) {
+      c0 = __ldg(z2 + i);
+      c1 = __ldg(z2 + i + stride);
+    }
+    double2 r0, r1;
+    r0.x = __dsub_rn(a0.x, __dmul_rn(h, b0.x));
+    r0.y = __dsub_rn(a0.y, __dmul_rn(h, b0.y));
+    r1.x = __dsub_rn(a1.x, __dmul_rn(h, b1.x));
+    r1.y = __dsub_rn(a1.y, __dmul_rn(h, b1.y));
+    w2[i] = r0;
+    w2[i + stride] = r1;
+    if (last) {
+      c0 = r0;
+      c1 = r1;
+    }
+    acc = __dadd_rn(acc, __dmul_rn(r0.x, c0.x));
+    acc = __dadd_rn(acc, __dmul_rn(r0.y, c0.y));
+    acc = __dadd_rn(acc, __dmul_rn(r1.x, c1.x));
+    acc = __dadd_rn(acc, __dmul_rn(r1.y, c1.y));
+  }
+  for (; i < n2; i += stride) {
+    const double2 a0 = w2[i];
+    const double2 b0 = __ldg(l2 + i);
+    double2 r0;
+    r0.x = __dsub_rn(a0.x, __dmul_rn(h, b0.x));
+    r0.y = __dsub_rn(a0.y, __dmul_rn(h, b0.y));
+    w2[i] = r0;
+    const double2 c0 = last ? r0 : __ldg(z2 + i);
+    acc = __dadd_rn(acc, __dmul_rn(r0.x, c0.x));
+    acc = __dadd_rn(acc, __dmul_rn(r0.y, c0.y));
+  }
+  if ((n & 1) && blockIdx.x == gridDim.x - 1 && threadIdx.x == blockDim.x - 1) {
+    const int64_t t = n - 1;
+    const double r = __dsub_rn(w[t], __dmul_rn(h, vl[t]));
+    w[t] = r;
+    acc = __dadd_rn(acc, __dmul_rn(r, last ? r : vn[t]));
+  }
+  const double s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+// Scalar variant (unaligned operands or lazily scaled inputs).
 __global__ void __launch_bounds__(kRedThreads)
     mgs_pass_kernel(KState *st, int ld, int l, int j, double *w, const double *vl,
                     const double *vl_scale, const double *vn, const double *vn_scale, int64_t n,
@@ -184,8 +250,7 @@ __global__ void __launch_bounds__(256)
     double acc = (first == 0) ? 0.0 : x[e];
     for (int l = first; l < hi; ++l) {
       const int q = l - first;
-      const double v = __ddiv_rn(a.vraw[q][e], st->vscale[l]);
-      const double xl = __dsub_rn(v, a.vt[q][ci]);
+      const double xl = __dsub_rn(a.v[q][e], a.vt[q][ci]);
       acc = __dadd_rn(acc, __dmul_rn(st->y[l], xl));
     }
     x[e] = acc;
@@ -251,6 +316,7 @@ int grid_for(int64_t n, int threads) {
 int launch_dot_partials(const double *a, const double *a_scale, const double *b,
                         const double *b_scale, int64_t n, double *partials, const int *live,
                         cudaStream_t s) {
+  prof::Scope scope(prof::kRed, (a == b ? 8.0 : 16.0) * (double)n, 0.0, s);
   dot_partials_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, a_scale, b, b_scale, n, partials,
                                                          live);
   PMK_LAUNCH_CHECK();
@@ -259,6 +325,7 @@ int launch_dot_partials(const double *a, const double *a_scale, const double *b,
 
 int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *partials,
                            cudaStream_t s) {
+  prof::Scope scope(prof::kRed, 16.0 * (double)n, 0.0, s);
   diffsq_partials_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, partials);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -266,6 +333,7 @@ int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *
 
 int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_sqrt,
                             cudaStream_t s) {
+  prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
   reduce_scalar_kernel<<<1, kRedThreads, 0, s>>>(partials, n, out, do_sqrt);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -273,6 +341,7 @@ int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_s
 
 int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
                  cudaStream_t s) {
+  prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
   begin_kernel<<<1, kRedThreads, 0, s>>>(st, partials, n_partials, parent_live);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -281,6 +350,14 @@ int launch_begin(KState *st, const double *partials, int n_partials, const int *
 int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *vl,
                     const double *vl_scale, const double *vn, const double *vn_scale, int64_t n,
                     const double *prev, int n_prev, double *partials, cudaStream_t s) {
+  prof::Scope scope(prof::kMGS, (vn ? 32.0 : 24.0) * (double)n, 0.0, s);
+  auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!vl_scale && !vn_scale && al(w) && al(vl) && (!vn || al(vn))) {
+    mgs_pass_vec_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, l, j, w, vl, vn, n, prev,
+                                                           n_prev, partials);
+    PMK_LAUNCH_CHECK();
+    return 0;
+  }
   mgs_pass_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, l, j, w, vl, vl_scale, vn, vn_scale,
                                                      n, prev, n_prev, partials);
   PMK_LAUNCH_CHECK();
@@ -289,12 +366,14 @@ int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *v
 
 int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
                       double tol, cudaStream_t s) {
+  prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
   finish_col_kernel<<<1, kRedThreads, 0, s>>>(st, ld, j, partials, n_partials, tol);
   PMK_LAUNCH_CHECK();
   return 0;
 }
 
 int launch_backsolve(KState *st, int ld, cudaStream_t s) {
+  prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
   backsolve_kernel<<<1, 32, 0, s>>>(st, ld);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -302,6 +381,10 @@ int launch_backsolve(KState *st, int ld, cudaStream_t s) {
 
 int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t n, int m, int nu,
                     int m_coarse, const int32_t *group_of, int first, cudaStream_t s) {
+  const double nc = (double)(n / m - 1) / nu + 1.0;  // coarse rows
+  prof::Scope scope(prof::kAsm,
+                    a.count * (8.0 * (double)n + 8.0 * nc * m_coarse) + (first ? 16.0 : 8.0) * n,
+                    0.0, s);
   assemble_kernel<<<grid_for(n, 256), 256, 0, s>>>(st, a, x, n, m, nu, m_coarse, group_of, first);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -309,6 +392,7 @@ int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t 
 
 int launch_restrict_time(const pmk_pair &P, const double *v, double *vh, cudaStream_t s) {
   const int64_t n = (int64_t)(P.n_T + 1) * P.m_fine;
+  prof::Scope scope(prof::kXfer, 8.0 * n + 8.0 * (double)(P.nu * P.n_T + 1) * P.m_fine, 0.0, s);
   restrict_time_kernel<<<grid_for(n, 256), 256, 0, s>>>(v, vh, P.nu, P.n_T, P.m_fine);
   PMK_LAUNCH_CHECK();
   return 0;
@@ -317,6 +401,7 @@ int launch_restrict_time(const pmk_pair &P, const double *v, double *vh, cudaStr
 int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, const int *live,
                      cudaStream_t s) {
   const int64_t n = (int64_t)(P.n_T + 1) * P.m_coarse;
+  prof::Scope scope(prof::kXfer, 8.0 * n + 8.0 * (double)(P.n_T + 1) * P.m_fine, 0.0, s);
   ts_gather_kernel<<<grid_for(n, 256), 256, 0, s>>>(fine, coarse, P.y_ptr, P.y_idx, P.y_val,
                                                     P.n_T + 1, P.m_fine, P.m_coarse, live);
   PMK_LAUNCH_CHECK();
@@ -325,6 +410,7 @@ int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, cons
 
 int launch_interpolate(const pmk_pair &P, const double *w, double *out, cudaStream_t s) {
   const int64_t n = (int64_t)(P.nu * P.n_T + 1) * P.m_fine;
+  prof::Scope scope(prof::kXfer, 8.0 * n + 8.0 * (double)(P.n_T + 1) * P.m_coarse, 0.0, s);
   interpolate_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, out, P.nu, P.n_T, P.m_fine, P.m_coarse,
                                                       P.group_of);
   PMK_LAUNCH_CHECK();

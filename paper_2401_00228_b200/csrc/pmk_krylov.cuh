@@ -25,7 +25,7 @@ struct KState {
 constexpr int kAsmChunk = 32;
 struct AssembleArgs {
   int count;
-  const double *vraw[kAsmChunk];
+  const double *v[kAsmChunk];  // normalised basis vectors
   const double *vt[kAsmChunk];
 };
 

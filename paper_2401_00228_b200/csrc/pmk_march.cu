@@ -24,6 +24,8 @@
 //   IMV  solver.py:349,359,403  x = v - interpolate(vt); w = A x; and the
 //                               partial dot(w, v_0) that seeds MGS
 //                               (solver.py:407, l = 0)
+#include <cstdlib>
+
 #include "pmk_internal.cuh"
 
 namespace pmk {
@@ -170,6 +172,7 @@ __global__ void __launch_bounds__(256)
           if (MODE == kModeMV) {
             p.out[e] = o;
           } else if (MODE == kModeMVR) {
+            if (p.v_norm_out) p.v_norm_out[e] = c;  // basis vector b/beta, w/h (solver.py:395,420)
             const double sv = __dsub_rn(o, __dmul_rn(p.mu, c));  // s -= mu * v
             if (k == 0) {
               p.vh[i] = sv;
@@ -203,7 +206,7 @@ struct Geometry {
 };
 
 template <int DIM, int MODE, int R, bool VAR>
-int run(const MarchParams &p, cudaStream_t s, int *n_partials) {
+int run(const MarchParams &p, cudaStream_t s, int *n_partials, double bytes, int cat) {
   auto kern = march_kernel<DIM, MODE, R, VAR>;
   static int occ = -1;
   if (occ < 0) {
@@ -230,7 +233,8 @@ int run(const MarchParams &p, cudaStream_t s, int *n_partials) {
   const int n_chunks = (int)((n_units + upc - 1) / upc);
   const int64_t n_items = (int64_t)tiles * n_chunks;
   const int grid = (int)(n_items < grid_cap ? n_items : grid_cap);
-  // BX threads per block, but launch_bounds 256 and shuffles need whole warps.
+  prof::Scope scope(cat, bytes, 0.0, s);
+  // BX threads per block (whole warps: the x-neighbours come from shuffles).
   march_kernel<DIM, MODE, R, VAR><<<grid, BX, 0, s>>>(p, BX, gx, gy, (int)upc, n_chunks);
   PMK_LAUNCH_CHECK();
   if (n_partials) *n_partials = grid;
@@ -238,26 +242,57 @@ int run(const MarchParams &p, cudaStream_t s, int *n_partials) {
 }
 
 template <int MODE>
-int dispatch(const MarchParams &p, cudaStream_t s, int *n_partials) {
+int dispatch(const MarchParams &p, cudaStream_t s, int *n_partials, double b, int c) {
   const bool var = p.P.var || p.Q.var;
   if (p.ny == 1) {
-    return var ? run<1, MODE, 1, true>(p, s, n_partials) : run<1, MODE, 1, false>(p, s, n_partials);
+    return var ? run<1, MODE, 1, true>(p, s, n_partials, b, c)
+               : run<1, MODE, 1, false>(p, s, n_partials, b, c);
   }
-  return var ? run<2, MODE, 2, true>(p, s, n_partials) : run<2, MODE, 8, false>(p, s, n_partials);
+  return var ? run<2, MODE, 2, true>(p, s, n_partials, b, c)
+             : run<2, MODE, 8, false>(p, s, n_partials, b, c);
+}
+
+// Algorithmic DRAM bytes of one launch.
+double march_bytes(int mode, const MarchParams &p, int *cat) {
+  const double N = (double)(p.n_steps + 1) * p.m;
+  if (mode == kModeMV) {
+    *cat = prof::kMV;
+    return 16.0 * N;
+  }
+  if (mode == kModeMVR) {
+    *cat = prof::kMVR;
+    double b = 8.0 * N + 8.0 * (double)(p.n_steps / p.nu + 1) * p.m;
+    if (p.v_norm_out) b += 8.0 * N;
+    return b;
+  }
+  *cat = prof::kIMV;
+  double b = 8.0 * N + 8.0 * (double)(p.n_steps / p.nu + 1) * p.m_coarse;
+  if (p.out) b += 8.0 * N;
+  if (p.x_out) b += 8.0 * N;
+  if (p.partials) b += 8.0 * N;
+  return b;
 }
 
 }  // namespace
 
 int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials) {
+  if (mode != kModeMV && mode != kModeMVR && mode != kModeIMV) return PMK_ERR_ARG;
+  int cat = 0;
+  const double bytes = march_bytes(mode, p, &cat);
+  static const bool force_reg = getenv("PMK_MARCH_REG") != nullptr;
+  if (!force_reg) {
+    int handled = 0;
+    const int rc = launch_march_tma(mode, p, s, n_partials, bytes, cat, &handled);
+    if (rc || handled) return rc;
+  }
   switch (mode) {
     case kModeMV:
-      return dispatch<kModeMV>(p, s, n_partials);
+      return dispatch<kModeMV>(p, s, n_partials, bytes, cat);
     case kModeMVR:
-      return dispatch<kModeMVR>(p, s, n_partials);
-    case kModeIMV:
-      return dispatch<kModeIMV>(p, s, n_partials);
+      return dispatch<kModeMVR>(p, s, n_partials, bytes, cat);
+    default:
+      return dispatch<kModeIMV>(p, s, n_partials, bytes, cat);
   }
-  return PMK_ERR_ARG;
 }
 
 }  // namespace pmk

@@ -1,0 +1,452 @@
+// pmk_march_tma.cu -- TMA-pipelined fused space-time stencil kernels
+// (K-MV, K-MVR, K-IMV; same semantics and rounding as pmk_march.cu).
+//
+// Data movement: every input space-time vector is described by a 1-D TMA
+// tensor map over its N doubles (out-of-range box elements are zero-filled,
+// so no end-of-array cases exist).  A box must start 16-byte aligned (an odd
+// fp64 coordinate raises an illegal-instruction fault on sm_100a), so each
+// row box is issued at the even coordinate at or below the row start and the
+// consumer applies the row's parity shift; a tile is therefore at most 255
+// columns wide (single tile) or 252 plus halo (wider rows).  A CTA owns a tile of R grid
+// rows x up to 256 columns and streams consecutive time slices of it through
+// an S-stage shared-memory ring: one elected thread issues, per slice, R+2
+// row boxes (256 doubles = 2 KB each; the rows above/below are the halo)
+// with cp.async.bulk.tensor, completion tracked by an mbarrier per stage.
+// The copy engine keeps S slices in flight per CTA while the threads
+// compute, which is what the register version lacked (it was latency- and
+// issue-bound at ~15% of HBM bandwidth).
+//
+// Compute per slice:
+//   pre-pass   each thread transforms one box column in place, once per
+//              element: v / scale (lazily normalised basis vector; the
+//              normalised value is also stored, solver.py:395/420) or
+//              v - Z vt (K-IMV; vt staged through the same ring);
+//   stencil    each thread walks its column down the R rows keeping the
+//              vertical neighbours in registers (3 shared loads per output),
+//              forms D^T u_k and B^T u_k in ascending column order with
+//              separately rounded products (bitwise the reference's scipy
+//              product), keeps B^T u_k in registers for slice k+1, and
+//              writes the mode's outputs with coalesced stores.
+#include <cuda.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "pmk_internal.cuh"
+
+namespace pmk {
+namespace {
+
+constexpr int kBox = 256;  // doubles per TMA box (one tile row)
+constexpr int kTmaThreads = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "PMK_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra PMK_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_row(double *dst, const CUtensorMap *map, int coord,
+                                        uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.1d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2}], [%3];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(coord), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Coef5 {
+  double s, w, c, e, n;
+};
+
+__device__ __forceinline__ Coef5 coef_at(const pmk_stencil &st, int64_t i, int m) {
+  if (!st.var) return Coef5{st.c[0], st.c[1], st.c[2], st.c[3], st.c[4]};
+  const double *c = st.coef;
+  return Coef5{__ldg(c + i), __ldg(c + m + i), __ldg(c + 2 * (int64_t)m + i),
+               __ldg(c + 3 * (int64_t)m + i), __ldg(c + 4 * (int64_t)m + i)};
+}
+
+__device__ __forceinline__ double stencil5(const Coef5 &a, bool hs, double vs, bool hw, double vw,
+                                           double vc, bool he, double ve, bool hn, double vn) {
+  double acc = 0.0;  // scipy csc_matvecs order: ascending column index
+  if (hs) acc = __dadd_rn(acc, __dmul_rn(a.s, vs));
+  if (hw) acc = __dadd_rn(acc, __dmul_rn(a.w, vw));
+  acc = __dadd_rn(acc, __dmul_rn(a.c, vc));
+  if (he) acc = __dadd_rn(acc, __dmul_rn(a.e, ve));
+  if (hn) acc = __dadd_rn(acc, __dmul_rn(a.n, vn));
+  return acc;
+}
+
+struct TmaGeom {
+  int single;  // 1: one column tile per row, box starts at x = 0
+  int tile_w;  // output columns per tile
+  int gx, gy;  // column tiles, row groups
+  int upc, n_chunks;
+};
+
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER>
+__global__ void __launch_bounds__(kTmaThreads)
+    march_tma_kernel(const MarchParams p, const __grid_constant__ CUtensorMap tm_v,
+                     const __grid_constant__ CUtensorMap tm_vt, const TmaGeom g) {
+  constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
+  constexpr int ROWS = (DIM == 2) ? R + 2 : 1;
+  constexpr int RO = (DIM == 2) ? R : 1;  // output rows per tile
+  // TMA tensor destinations must be 128-byte aligned; dynamic shared memory
+  // follows the static part at an unspecified alignment, so align by hand.
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double *smem = reinterpret_cast<double *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
+  __shared__ __align__(8) uint64_t bars[S];
+
+  if (!is_live(p.live)) return;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int nx = p.nx, ny = p.ny, m = p.m;
+  const int U = (MODE == kModeMVR) ? p.nu : 1;
+  const int n_units = p.n_steps / U + 1;
+  const int tiles = g.gx * g.gy;
+  const int64_t n_items = (int64_t)tiles * g.n_chunks;
+  const double vsc = p.v_scale ? *p.v_scale : 1.0;
+  const double v0sc = (MODE == kModeIMV && p.v0_scale) ? *p.v0_scale : 1.0;
+  double dot = 0.0;
+  uint32_t it = 0;  // slices consumed by this CTA (ring position)
+
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int tile = (int)(item % tiles);
+    const int chunk = (int)(item / tiles);
+    const int x0 = (tile % g.gx) * g.tile_w;
+    const int y0 = (DIM == 2) ? (tile / g.gx) * R : 0;
+    const int U0 = chunk * g.upc;
+    const int U1 = min(n_units, U0 + g.upc);
+    const int kb = (U0 == 0) ? 0 : U * (U0 - 1) + 1;
+    const int ke = U * (U1 - 1) + 1;
+    const int kstart = (kb > 0) ? kb - 1 : 0;
+    const int nsl = ke - kstart;
+    const int boxx = g.single ? 0 : x0 - 1;  // grid column of box element 0
+
+    // rows of the tile that exist
+    int rlo = 0, rhi = ROWS - 1;
+    if (DIM == 2) {
+      if (y0 - 1 < 0) rlo = 1;
+      if (y0 - 1 + rhi > ny - 1) rhi = ny - 1 - (y0 - 1);
+    }
+    const uint32_t tx_bytes = (uint32_t)(NB * (rhi - rlo + 1) * kBox * sizeof(double));
+
+    auto issue = [&](int k, int stage) {
+      double *sv = smem + (size_t)stage * NB * ROWS * kBox;
+      mbar_expect_tx(&bars[stage], tx_bytes);
+      const int K = (k == 0) ? 0 : (k - 1) / p.nu + 1;
+      for (int r = rlo; r <= rhi; ++r) {
+        const int y = (DIM == 2) ? y0 - 1 + r : 0;
+        const int c = (int)((int64_t)k * m + (int64_t)y * nx + boxx);
+        tma_row(sv + r * kBox, &tm_v, c & ~1, &bars[stage]);
+        if (NB == 2) {
+          const int cv = (int)((int64_t)K * p.m_coarse + (int64_t)y * nx + boxx);
+          tma_row(sv + (ROWS + r) * kBox, &tm_vt, cv & ~1, &bars[stage]);
+        }
+      }
+    };
+    if (t == 0) {
+      const int pre = nsl < S ? nsl : S;
+      for (int q = 0; q < pre; ++q) issue(kstart + q, (int)((it + q) % S));
+    }
+
+    // this thread's output column
+    const int x = g.single ? t : x0 + t;
+    const bool xin = (g.single ? t < nx : t < g.tile_w) && x < nx;
+    const bool hw = x > 0, he = x < nx - 1;
+    // this thread's pre-pass grid column (box element t + row shift)
+    const int px = boxx + t;
+    const bool pin = t < kBox - 1 && px >= 0 && px < nx;
+    const int xo = x - boxx;  // box offset of this thread's output column
+
+    double qprev[RO], acc[RO];
+#pragma unroll
+    for (int r = 0; r < RO; ++r) {
+      qprev[r] = 0.0;
+      acc[r] = 0.0;
+    }
+    Coef5 pcst, qcst;
+    if (!VAR) {
+      pcst = Coef5{p.P.c[0], p.P.c[1], p.P.c[2], p.P.c[3], p.P.c[4]};
+      qcst = Coef5{p.Q.c[0], p.Q.c[1], p.Q.c[2], p.Q.c[3], p.Q.c[4]};
+    }
+
+    for (int i = 0; i < nsl; ++i, ++it) {
+      const int k = kstart + i;
+      const bool prime = k < kb;
+      const int stage = (int)(it % S);
+      double *sv = smem + (size_t)stage * NB * ROWS * kBox;
+      const int K = (k == 0) ? 0 : (k - 1) / p.nu + 1;
+      // IMV: start the v_0 loads of the dot early
+      double v0v[RO];
+      if (MODE == kModeIMV && p.partials && !prime && xin) {
+#pragma unroll
+        for (int r = 0; r < RO; ++r) {
+          const int y = y0 + r;
+          v0v[r] = (y < ny) ? __ldg(p.v0 + (int64_t)k * m + (int64_t)y * nx + x) : 0.0;
+        }
+      }
+      // parity shift of grid row y inside its box (see issue())
+      const int pk = (int)(((int64_t)k * m + boxx) & 1);
+      const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
+      auto sh = [&](int y) { return (pk + (y & nx)) & 1; };
+      auto shK = [&](int y) { return (pK + (y & nx)) & 1; };
+      mbar_wait(&bars[stage], (it / S) & 1);
+      // ---------------- pre-pass: u = v / scale  or  u = v - Z vt
+      if ((p.v_scale || MODE == kModeIMV) && pin) {
+        for (int r = rlo; r <= rhi; ++r) {
+          const int y = (DIM == 2) ? y0 - 1 + r : 0;
+          double *cell = sv + r * kBox + t + sh(y);
+          double u = *cell;
+          if (p.v_scale) u = __ddiv_rn(u, vsc);
+          if (MODE == kModeIMV) {
+            double z;
+            if (GATHER)
+              z = __ldg(p.vt + (int64_t)K * p.m_coarse + p.group_of[(int64_t)y * nx + px]);
+            else
+              z = sv[(ROWS + r) * kBox + t + shK(y)];
+            u = __dsub_rn(u, z);
+          }
+          *cell = u;
+        }
+      }
+      if (p.v_scale || MODE == kModeIMV) __syncthreads();
+      // ---------------- stencil pass down this thread's column
+      if (xin) {
+        const double *col = sv + xo;
+        double up = (DIM == 2 && rlo == 0) ? col[sh(y0 - 1)] : 0.0;
+        double cur = col[((DIM == 2) ? kBox : 0) + sh(y0)];
+        const bool drop = p.dropped && p.dropped[k];
+#pragma unroll
+        for (int r = 0; r < RO; ++r) {
+          const int y = y0 + r;
+          if (DIM == 2 && y >= ny) break;
+          const int br = (DIM == 2) ? r + 1 : 0;  // box row of y
+          const bool hs = DIM == 2 && y > 0;
+          const bool hn = DIM == 2 && y < ny - 1;
+          const double *row = col + br * kBox + sh(y);
+          const double dn = hn ? col[(br + 1) * kBox + sh(y + 1)] : 0.0;
+          const double lf = hw ? row[-1] : 0.0;
+          const double rt = he ? row[1] : 0.0;
+          const int64_t gi = (int64_t)y * nx + x;
+          Coef5 a, b;
+          if (VAR) {
+            a = coef_at(p.P, gi, m);
+            b = coef_at(p.Q, gi, m);
+          } else {
+            a = pcst;
+            b = qcst;
+          }
+          const double Pu = stencil5(a, hs, up, hw, lf, cur, he, rt, hn, dn);
+          const double Qu = stencil5(b, hs, up, hw, lf, cur, he, rt, hn, dn);
+          if (!prime) {
+            double o;
+            if (k == 0) {
+              o = cur;  // identity block row (stepper.py:100)
+            } else {
+              o = __dsub_rn(Pu, qprev[r]);
+              if (drop) o = __dadd_rn(o, qprev[r]);  // stepper.py:103-104
+            }
+            const int64_t e = (int64_t)k * m + gi;
+            if (MODE == kModeMV) {
+              p.out[e] = o;
+            } else if (MODE == kModeMVR) {
+              if (p.v_norm_out) p.v_norm_out[e] = cur;
+              const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
+              if (k == 0) {
+                p.vh[gi] = sval;
+              } else {
+                const int pos = (k - 1) % p.nu;
+                acc[r] = (pos == 0) ? sval : __dadd_rn(acc[r], sval);
+                if (pos == p.nu - 1) p.vh[(int64_t)((k - 1) / p.nu + 1) * m + gi] = acc[r];
+              }
+            } else {
+              if (p.x_out) p.x_out[e] = cur;
+              if (p.out) p.out[e] = o;
+              if (p.partials) {
+                double z = v0v[r];
+                if (p.v0_scale) z = __ddiv_rn(z, v0sc);
+                dot = __dadd_rn(dot, __dmul_rn(o, z));
+              }
+            }
+          }
+          qprev[r] = Qu;
+          up = cur;
+          cur = dn;
+        }
+      }
+      __syncthreads();  // stage fully consumed
+      if (t == 0 && i + S < nsl) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(k + S, stage);
+      }
+    }
+  }
+  if (MODE == kModeIMV && p.partials) {
+    const double s = block_sum(dot);
+    if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  return fn;
+}
+
+bool encode_1d(CUtensorMap *map, const double *base, int64_t n) {
+  EncodeTiledFn fn = encoder();
+  if (!fn || !base || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  cuuint64_t dims[1] = {(cuuint64_t)n};
+  cuuint64_t strides[1] = {0};
+  cuuint32_t box[1] = {kBox};
+  cuuint32_t estr[1] = {1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<double *>(base), dims, strides,
+            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER>
+int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
+            int *n_partials, double bytes, int cat) {
+  constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
+  constexpr int ROWS = (DIM == 2) ? R + 2 : 1;
+  const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
+  auto kern = march_tma_kernel<MODE, DIM, R, S, VAR, GATHER>;
+  static int occ = -1;
+  if (occ < 0) {
+    PMK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int b = 0;
+    PMK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, kTmaThreads, smem));
+    occ = b > 0 ? b : 1;
+  }
+  TmaGeom g;
+  g.single = p.nx <= kBox - 1 ? 1 : 0;  // row + parity shift fits one box
+  g.tile_w = g.single ? p.nx : kBox - 4;  // halo + shift fit one box
+  g.gx = (p.nx + g.tile_w - 1) / g.tile_w;
+  g.gy = (DIM == 2) ? (p.ny + R - 1) / R : 1;
+  const int U = (MODE == kModeMVR) ? p.nu : 1;
+  const int n_units = p.n_steps / U + 1;
+  const int tiles = g.gx * g.gy;
+  int grid_cap = occ * kSMs;
+  if (MODE == kModeIMV && grid_cap > kMaxPartials) grid_cap = kMaxPartials;
+  // ~8 work items per resident CTA; chunks of at most 32 units (one extra
+  // prime slice per chunk, served from L2).
+  int64_t upc = ((int64_t)n_units * tiles) / (8LL * grid_cap);
+  if (upc < 2) upc = 2;
+  if (upc > 32) upc = 32;
+  g.upc = (int)upc;
+  g.n_chunks = (int)((n_units + upc - 1) / upc);
+  const int64_t n_items = (int64_t)tiles * g.n_chunks;
+  const int grid = (int)(n_items < grid_cap ? n_items : grid_cap);
+  static const bool dbg = getenv("PMK_DEBUG") != nullptr;
+  if (dbg)
+    fprintf(stderr, "[pmk] tma mode %d dim %d R %d S %d var %d gather %d: nx %d ny %d steps %d "
+            "grid %d smem %zu occ %d single %d tile_w %d gx %d gy %d upc %d chunks %d\n",
+            MODE, DIM, R, S, (int)VAR, (int)GATHER, p.nx, p.ny, p.n_steps, grid, smem, occ,
+            g.single, g.tile_w, g.gx, g.gy, g.upc, g.n_chunks);
+  prof::Scope scope(cat, bytes, 0.0, s);
+  kern<<<grid, kTmaThreads, smem, s>>>(p, mv, mvt, g);
+  PMK_LAUNCH_CHECK();
+  if (n_partials) *n_partials = grid;
+  return 0;
+}
+
+}  // namespace
+
+// Returns 1 when the TMA path handled the launch, 0 when the caller should
+// use the register path (no driver entry point, unaligned base, N >= 2^31).
+int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_partials,
+                     double bytes, int cat, int *handled) {
+  *handled = 0;
+  const int64_t N = (int64_t)(p.n_steps + 1) * p.m;
+  if (N + 2 * kBox >= (int64_t)1 << 31) return 0;
+  CUtensorMap mv, mvt;
+  if (!encode_1d(&mv, p.v, N)) return 0;
+  const bool gather = (mode == kModeIMV) && p.group_of != nullptr;
+  if (mode == kModeIMV && !gather) {
+    const int64_t Nc = (int64_t)(p.n_steps / p.nu + 1) * p.m_coarse;
+    if (!encode_1d(&mvt, p.vt, Nc)) return 0;
+  } else {
+    mvt = mv;
+  }
+  const bool var = p.P.var || p.Q.var;
+  const bool d2 = p.ny > 1;
+  int rc = 0;
+#define PMK_RUN(MODE, DIM, R, S, VAR, GATHER) \
+  rc = run_tma<MODE, DIM, R, S, VAR, GATHER>(p, mv, mvt, s, n_partials, bytes, cat)
+  switch (mode) {
+    case kModeMV:
+      if (d2) {
+        if (var) PMK_RUN(kModeMV, 2, 8, 3, true, false); else PMK_RUN(kModeMV, 2, 8, 3, false, false);
+      } else {
+        if (var) PMK_RUN(kModeMV, 1, 1, 8, true, false); else PMK_RUN(kModeMV, 1, 1, 8, false, false);
+      }
+      break;
+    case kModeMVR:
+      if (d2) {
+        if (var) PMK_RUN(kModeMVR, 2, 8, 3, true, false); else PMK_RUN(kModeMVR, 2, 8, 3, false, false);
+      } else {
+        if (var) PMK_RUN(kModeMVR, 1, 1, 8, true, false); else PMK_RUN(kModeMVR, 1, 1, 8, false, false);
+      }
+      break;
+    case kModeIMV:
+      if (d2) {
+        if (gather) {
+          if (var) PMK_RUN(kModeIMV, 2, 8, 3, true, true); else PMK_RUN(kModeIMV, 2, 8, 3, false, true);
+        } else {
+          if (var) PMK_RUN(kModeIMV, 2, 8, 2, true, false); else PMK_RUN(kModeIMV, 2, 8, 2, false, false);
+        }
+      } else {
+        if (gather) {
+          if (var) PMK_RUN(kModeIMV, 1, 1, 8, true, true); else PMK_RUN(kModeIMV, 1, 1, 8, false, true);
+        } else {
+          if (var) PMK_RUN(kModeIMV, 1, 1, 8, true, false); else PMK_RUN(kModeIMV, 1, 1, 8, false, false);
+        }
+      }
+      break;
+    default:
+      return PMK_ERR_ARG;
+  }
+#undef PMK_RUN
+  if (rc == 0) *handled = 1;
+  return rc;
+}
+
+}  // namespace pmk

@@ -326,20 +326,21 @@ def _setup_native(hier: LevelHierarchy) -> None:
             ts = _empty((lvl.pair.n_T + 1) * lvl.pair.n)
         if idx == 0:
             rhs = hier.fine.rhs.reshape(-1)
-            ws, cos = [], []
+            vs, cos, wb = [], [], None
         else:
             rhs = _empty(lvl.total_dim)
-            ws = [_empty(lvl.total_dim) for _ in range(lvl.budget)]
+            vs = [_empty(lvl.total_dim) for _ in range(lvl.budget)]
             cos = [_empty(nxt.total_dim) for _ in range(lvl.budget)]
-        keep += [rhs, ws, cos, ts]
-        n = len(ws)
-        arr_w = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in ws])
+            wb = _empty(lvl.total_dim)
+        keep += [rhs, vs, cos, wb, ts]
+        n = len(vs)
+        arr_v = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in vs])
         arr_c = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in cos])
-        _lib.check(lib.pmk_hier_set_buffers(H, idx, _lib.ptr(rhs), arr_w, arr_c, n,
-                                            _lib.ptr(ts)), "set_buffers")
+        _lib.check(lib.pmk_hier_set_buffers(H, idx, _lib.ptr(rhs), arr_v, arr_c, n,
+                                            _lib.ptr(wb), _lib.ptr(ts)), "set_buffers")
     crhs = _empty(hier.levels[-1].total_dim)
     keep.append(crhs)
-    _lib.check(lib.pmk_hier_set_buffers(H, L - 1, _lib.ptr(crhs), None, None, 0, None),
+    _lib.check(lib.pmk_hier_set_buffers(H, L - 1, _lib.ptr(crhs), None, None, 0, None, None),
                "set_buffers")
 
 
@@ -418,16 +419,18 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
     st = _state(hier, level_idx)
     if st["beta"] == 0.0:
         return torch.zeros_like(b), report
-    ws, cos = [], []
+    vs, cos = [], []
     per_iter = 8 * (lvl.total_dim + nxt.total_dim)
+    _check_memory(8 * lvl.total_dim)
+    w = _empty(lvl.total_dim)  # unnormalised new vector, reused every iteration
     for j in range(max_iter):
         _check_memory(per_iter)
-        w = _empty(lvl.total_dim)
+        v = _empty(lvl.total_dim)
         co = _empty(nxt.total_dim)
-        ws.append(w)
+        vs.append(v)
         cos.append(co)
-        _lib.check(lib.pmk_fgmres_step(H, level_idx, j, _lib.ptr(w), _lib.ptr(co), s),
-                   "fgmres_step")
+        _lib.check(lib.pmk_fgmres_step(H, level_idx, j, _lib.ptr(v), _lib.ptr(w), _lib.ptr(co),
+                                       s), "fgmres_step")
         if tol is not None:
             st = _state(hier, level_idx)
             if st["breakdown"] or st["rel"] <= tol:
@@ -441,19 +444,14 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
     if st["breakdown"] or (tol is not None and n_iter and report.residual_history[-1] <= tol):
         report.converged = True
     if keep_basis:
-        scales = [st["beta"]] + [st["hraw"][l, l - 1] for l in range(1, n_iter + 1)]
-        raws = [b] + ws
-        n_basis = n_iter if st["breakdown"] else n_iter + 1
-        basis = [(raws[l] / scales[l]).cpu().numpy() for l in range(n_basis)]
-        pre = []
-        for l in range(n_iter):
-            vl = raws[l] / scales[l]
-            t = lvl.pair.interpolate(cos[l])
-            pre.append((vl - t).cpu().numpy())
+        basis = [vs[l].cpu().numpy() for l in range(n_iter)]
+        if not st["breakdown"]:
+            basis.append((w / st["hraw"][n_iter, n_iter - 1]).cpu().numpy())
+        pre = [(vs[l] - lvl.pair.interpolate(cos[l])).cpu().numpy() for l in range(n_iter)]
         report.metadata["basis"] = basis
         report.metadata["preconditioned"] = pre
         report.metadata["hessenberg"] = st["hraw"][:n_iter + 1, :n_iter].copy()
-    del ws, cos
+    del vs, cos, w
     return x, report
 
 
@@ -507,7 +505,8 @@ def _nrm2(t) -> float:
     return float(out.item())
 
 
-def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | None = None):
+def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | None = None,
+           out=None):
     import torch
 
     cfg = hier.config
@@ -526,6 +525,9 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     report.metadata["true_relative_residual"] = true_res
     report.converged = true_res <= cfg.tol
     report.level_stats = {"levels": hier.describe(), "moves": hier.moves}
+    if out is not None:
+        out.copy_(x.reshape(out.shape))  # e.g. into a pinned host buffer
+        return out, report
     if output is None:
         output = "host" if hier.fine.host_io else "device"
     if output == "host":
@@ -533,14 +535,17 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     return x, report
 
 
-def two_level_solve(hier: LevelHierarchy, ledger=None, model=None, output: str | None = None):
+def two_level_solve(hier: LevelHierarchy, ledger=None, model=None, output: str | None = None,
+                    out=None):
     if hier.n_levels != 2:
         raise ValueError("two_level_solve expects a 2-level hierarchy")
-    return _solve(hier, ledger, model, "two_level", output)
+    return _solve(hier, ledger, model, "two_level", output, out)
 
 
-def multilevel_solve(hier: LevelHierarchy, ledger=None, model=None, output: str | None = None):
+def multilevel_solve(hier: LevelHierarchy, ledger=None, model=None, output: str | None = None,
+                     out=None):
     """Outer FGMRES to cfg.tol (reference solver.py:459-488).  Returns x as
     numpy when the fine system was built from a numpy u0, else as a device
-    tensor (``output`` = "host" / "device" overrides)."""
-    return _solve(hier, ledger, model, f"multilevel[{hier.n_levels}]", output)
+    tensor (``output`` = "host" / "device" overrides; ``out`` = a tensor,
+    e.g. pinned host memory, that receives x)."""
+    return _solve(hier, ledger, model, f"multilevel[{hier.n_levels}]", output, out)

@@ -167,3 +167,58 @@ def test_bad_shapes_raise():
         h.levels[0].system.matvec(np.zeros(7))
     with pytest.raises(ValueError):
         P.apply_preconditioner(h, 2, np.zeros(h.levels[2].total_dim))
+
+
+@pytest.mark.parametrize("dim,nx,ny,n_t,theta", [(1, 1023, 1, 16, 0.5), (2, 300, 20, 8, 0.5),
+                                                 (2, 255, 9, 6, 1.0), (1, 255, 1, 12, 0.5),
+                                                 (2, 256, 5, 4, 0.5), (1, 17, 1, 9, 0.3)])
+def test_fused_kernels_bitwise_wide_and_odd_grids(dim, nx, ny, n_t, theta):
+    """K-MV, K-MVR (shift + restrict + normalised copy) and K-IMV against the
+    oracle's operations, on grids wider than one 255-column tile and with odd
+    row lengths (TMA parity shifts)."""
+    import ctypes
+
+    import torch
+
+    from oracle import pintmk_oracle as O
+    from paper_2401_00228_b200 import _lib
+    from paper_2401_00228_b200.intergrid import TimePair
+    from paper_2401_00228_b200.stepper import BlockBidiagonalSystem
+
+    a, _ = O.laplacian(dim, nx, ny)
+    d, b = O.blocks_from(a, theta, 1e-4)
+    nu = 2 if n_t % 2 == 0 else 3 if n_t % 3 == 0 else 1
+    sysd = BlockBidiagonalSystem(d, b, n_t, grid=(nx, ny), dim=dim)
+    so = O.System(d, b, n_t)
+    pair = TimePair(nx * ny, nu, n_t // nu)
+    po = O.Pair(nu, n_t // nu, nx * ny)
+    rng = np.random.default_rng(5)
+    v = rng.standard_normal(so.size)
+    scale = 3.7
+    # K-MV
+    np.testing.assert_array_equal(sysd.matvec(v), O.matvec(so, v))
+    # K-MVR with lazy scale: vh = restrict(A v - mu v), v_norm = raw / scale
+    lib = _lib.load()
+    raw = torch.from_numpy(v * scale).cuda()
+    sc = torch.tensor([scale], dtype=torch.float64, device="cuda")
+    vh = torch.empty((n_t // nu + 1) * nx * ny, dtype=torch.float64, device="cuda")
+    _lib.check(lib.pmk_stmv_shift_restrict(ctypes.byref(sysd.level_desc()),
+                                           ctypes.byref(pair._pair_desc()), 0.75, _lib.ptr(raw),
+                                           _lib.ptr(sc), _lib.ptr(vh), None, _lib.stream_ptr()),
+               "mvr")
+    vn = (v * scale) / scale
+    s_ref = O.matvec(so, vn)
+    s_ref -= 0.75 * vn
+    np.testing.assert_array_equal(vh.cpu().numpy(), O.restrict(po, s_ref))
+    # K-IMV: x = v - Z vt, w = A x
+    vt = rng.standard_normal((n_t // nu + 1) * nx * ny)
+    x = torch.empty(so.size, dtype=torch.float64, device="cuda")
+    w = torch.empty_like(x)
+    vd = torch.from_numpy(v).cuda()
+    _lib.check(lib.pmk_interp_sub_stmv(ctypes.byref(sysd.level_desc()),
+                                       ctypes.byref(pair._pair_desc()), _lib.ptr(vd), None,
+                                       _lib.ptr(torch.from_numpy(vt).cuda()), _lib.ptr(x),
+                                       _lib.ptr(w), _lib.stream_ptr()), "imv")
+    xr = v - O.interpolate(po, vt)
+    np.testing.assert_array_equal(x.cpu().numpy(), xr)
+    np.testing.assert_array_equal(w.cpu().numpy(), O.matvec(so, xr))
