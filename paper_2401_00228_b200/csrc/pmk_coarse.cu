@@ -216,9 +216,11 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     if (ny == 1) {
       int rc = gemm(rows, nx, nx, rhs, nx, 0, C.sx, nx, 0, C.work0, nx, 0, 1, live, s);
       if (rc) return rc;
-      prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
-      dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta, C.dropped,
-                                                           C.n_steps, m, live);
+      {
+        prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
+        dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta,
+                                                             C.dropped, C.n_steps, m, live);
+      }
       PMK_LAUNCH_CHECK();
       rc = gemm(rows, nx, nx, C.work0, nx, 0, C.sx, nx, 0, out, nx, 0, 1, live, s);
       if (rc) return rc;
@@ -230,9 +232,11 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       // S_y X_k per slice
       rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work0, nx, m, C.work1, nx, m, rows, live, s);
       if (rc) return rc;
-      prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
-      dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta, C.dropped,
-                                                           C.n_steps, m, live);
+      {
+        prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
+        dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta,
+                                                             C.dropped, C.n_steps, m, live);
+      }
       PMK_LAUNCH_CHECK();
       rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work1, nx, m, C.work0, nx, m, rows, live, s);
       if (rc) return rc;
@@ -257,9 +261,11 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     const int cb = (m + 255) / 256 < 4 * kSMs ? (m + 255) / 256 : 4 * kSMs;
     const int gb = (m * 32 + 255) / 256;
     for (int k = 1; k <= C.n_steps; ++k) {
-      prof::Scope c1(prof::kCoarseMisc, 32.0 * m, 0.0, s);
-      coupling_kernel<<<cb, 256, 0, s>>>(rhs + (int64_t)k * m, out + (int64_t)(k - 1) * m,
+      {
+        prof::Scope c1(prof::kCoarseMisc, 32.0 * m, 0.0, s);
+        coupling_kernel<<<cb, 256, 0, s>>>(rhs + (int64_t)k * m, out + (int64_t)(k - 1) * m,
                                          C.work0, C.coupling, nx, ny, C.dropped, k, live);
+      }
       PMK_LAUNCH_CHECK();
       prof::Scope c2(prof::kCoarseMisc, 8.0 * m * (double)m + 16.0 * m, 2.0 * m * (double)m, s);
       gemv_kernel<<<gb, 256, 0, s>>>(C.dinv, C.work0, out + (int64_t)k * m, m, live);

@@ -100,7 +100,7 @@ struct TmaGeom {
   int upc, n_chunks;
 };
 
-template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER>
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED>
 __global__ void __launch_bounds__(kTmaThreads)
     march_tma_kernel(const MarchParams p, const __grid_constant__ CUtensorMap tm_v,
                      const __grid_constant__ CUtensorMap tm_vt, const TmaGeom g) {
@@ -127,8 +127,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int n_units = p.n_steps / U + 1;
   const int tiles = g.gx * g.gy;
   const int64_t n_items = (int64_t)tiles * g.n_chunks;
-  const double vsc = p.v_scale ? *p.v_scale : 1.0;
-  const double v0sc = (MODE == kModeIMV && p.v0_scale) ? *p.v0_scale : 1.0;
+  const double vsc = SCALED ? *p.v_scale : 1.0;
   double dot = 0.0;
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -179,7 +178,6 @@ __global__ void __launch_bounds__(kTmaThreads)
     // this thread's pre-pass grid column (box element t + row shift)
     const int px = boxx + t;
     const bool pin = t < kBox - 1 && px >= 0 && px < nx;
-    const int xo = x - boxx;  // box offset of this thread's output column
 
     double qprev[RO], acc[RO];
 #pragma unroll
@@ -193,74 +191,86 @@ __global__ void __launch_bounds__(kTmaThreads)
       qcst = Coef5{p.Q.c[0], p.Q.c[1], p.Q.c[2], p.Q.c[3], p.Q.c[4]};
     }
 
+    const int nu = p.nu;
+    const int xo = x - boxx;         // box offset of this thread's output column
+    const int gx0 = y0 * nx + x;     // in-slice index of (y0, x)
     for (int i = 0; i < nsl; ++i, ++it) {
+      // ---- per-slice uniform quantities
       const int k = kstart + i;
       const bool prime = k < kb;
       const int stage = (int)(it % S);
       double *sv = smem + (size_t)stage * NB * ROWS * kBox;
-      const int K = (k == 0) ? 0 : (k - 1) / p.nu + 1;
+      const int K = (k == 0) ? 0 : (k - 1) / nu + 1;  // coarse slice of k
+      const int pos = (k == 0) ? nu - 1 : (k - 1) - (K - 1) * nu;
+      const bool drop = p.dropped && p.dropped[k];
+      const int pk = (int)(((int64_t)k * m + boxx) & 1);  // row parity shifts (issue())
+      const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
+      const int64_t kofs = (int64_t)k * m;
       // IMV: start the v_0 loads of the dot early
       double v0v[RO];
       if (MODE == kModeIMV && p.partials && !prime && xin) {
+        const double *v0k = p.v0 + kofs + gx0;
 #pragma unroll
-        for (int r = 0; r < RO; ++r) {
-          const int y = y0 + r;
-          v0v[r] = (y < ny) ? __ldg(p.v0 + (int64_t)k * m + (int64_t)y * nx + x) : 0.0;
-        }
+        for (int r = 0; r < RO; ++r) v0v[r] = (y0 + r < ny) ? __ldg(v0k + r * nx) : 0.0;
       }
-      // parity shift of grid row y inside its box (see issue())
-      const int pk = (int)(((int64_t)k * m + boxx) & 1);
-      const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
-      auto sh = [&](int y) { return (pk + (y & nx)) & 1; };
-      auto shK = [&](int y) { return (pK + (y & nx)) & 1; };
       mbar_wait(&bars[stage], (it / S) & 1);
-      // ---------------- pre-pass: u = v / scale  or  u = v - Z vt
-      if ((p.v_scale || MODE == kModeIMV) && pin) {
-        for (int r = rlo; r <= rhi; ++r) {
+      // ---- pre-pass: u = v / scale  or  u = v - Z vt, once per element
+      if ((SCALED || MODE == kModeIMV) && pin) {
+        const double *vtk = GATHER ? p.vt + (int64_t)K * p.m_coarse : nullptr;
+#pragma unroll
+        for (int r = 0; r < ROWS; ++r) {
+          if (r < rlo || r > rhi) continue;
           const int y = (DIM == 2) ? y0 - 1 + r : 0;
-          double *cell = sv + r * kBox + t + sh(y);
+          double *cell = sv + r * kBox + t + ((pk + (y & nx)) & 1);
           double u = *cell;
-          if (p.v_scale) u = __ddiv_rn(u, vsc);
+          // 0 / scale = 0 (scale > 0): skipping it keeps exact zeros (the
+          // first Krylov vector is mostly zero) off the division slow path
+          if (SCALED && u != 0.0) u = __ddiv_rn(u, vsc);
           if (MODE == kModeIMV) {
-            double z;
-            if (GATHER)
-              z = __ldg(p.vt + (int64_t)K * p.m_coarse + p.group_of[(int64_t)y * nx + px]);
-            else
-              z = sv[(ROWS + r) * kBox + t + shK(y)];
+            const double z = GATHER ? __ldg(vtk + p.group_of[y * nx + px])
+                                    : sv[(ROWS + r) * kBox + t + ((pK + (y & nx)) & 1)];
             u = __dsub_rn(u, z);
           }
           *cell = u;
         }
       }
-      if (p.v_scale || MODE == kModeIMV) __syncthreads();
-      // ---------------- stencil pass down this thread's column
+      if (SCALED || MODE == kModeIMV) __syncthreads();
+      // ---- stencil pass down this thread's column.  Absent neighbours read
+      // as 0: adding their (+-0) products to the partial sum leaves it
+      // unchanged, so the sum equals the reference's sparse product.
       if (xin) {
         const double *col = sv + xo;
-        double up = (DIM == 2 && rlo == 0) ? col[sh(y0 - 1)] : 0.0;
-        double cur = col[((DIM == 2) ? kBox : 0) + sh(y0)];
-        const bool drop = p.dropped && p.dropped[k];
+        double up = (DIM == 2 && rlo == 0) ? col[(pk + ((y0 - 1) & nx)) & 1] : 0.0;
+        double cur = col[((DIM == 2) ? kBox : 0) + ((pk + (y0 & nx)) & 1)];
 #pragma unroll
         for (int r = 0; r < RO; ++r) {
           const int y = y0 + r;
           if (DIM == 2 && y >= ny) break;
-          const int br = (DIM == 2) ? r + 1 : 0;  // box row of y
-          const bool hs = DIM == 2 && y > 0;
-          const bool hn = DIM == 2 && y < ny - 1;
-          const double *row = col + br * kBox + sh(y);
-          const double dn = hn ? col[(br + 1) * kBox + sh(y + 1)] : 0.0;
+          const double *row = col + ((DIM == 2) ? (r + 1) * kBox : 0) + ((pk + (y & nx)) & 1);
+          const double dn = (DIM == 2 && y < ny - 1)
+                                ? col[(r + 2) * kBox + ((pk + ((y + 1) & nx)) & 1)]
+                                : 0.0;
           const double lf = hw ? row[-1] : 0.0;
           const double rt = he ? row[1] : 0.0;
-          const int64_t gi = (int64_t)y * nx + x;
           Coef5 a, b;
           if (VAR) {
-            a = coef_at(p.P, gi, m);
-            b = coef_at(p.Q, gi, m);
+            a = coef_at(p.P, gx0 + r * nx, m);
+            b = coef_at(p.Q, gx0 + r * nx, m);
           } else {
             a = pcst;
             b = qcst;
           }
-          const double Pu = stencil5(a, hs, up, hw, lf, cur, he, rt, hn, dn);
-          const double Qu = stencil5(b, hs, up, hw, lf, cur, he, rt, hn, dn);
+          double Pu = __dmul_rn(a.s, up), Qu = __dmul_rn(b.s, up);
+          if (DIM == 1) {  // no S term in 1-D: start from the W product
+            Pu = 0.0;
+            Qu = 0.0;
+          }
+          Pu = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(Pu, __dmul_rn(a.w, lf)), __dmul_rn(a.c, cur)),
+                                   __dmul_rn(a.e, rt)),
+                         __dmul_rn(a.n, dn));
+          Qu = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(Qu, __dmul_rn(b.w, lf)), __dmul_rn(b.c, cur)),
+                                   __dmul_rn(b.e, rt)),
+                         __dmul_rn(b.n, dn));
           if (!prime) {
             double o;
             if (k == 0) {
@@ -269,26 +279,19 @@ __global__ void __launch_bounds__(kTmaThreads)
               o = __dsub_rn(Pu, qprev[r]);
               if (drop) o = __dadd_rn(o, qprev[r]);  // stepper.py:103-104
             }
-            const int64_t e = (int64_t)k * m + gi;
+            const int gi = gx0 + r * nx;
             if (MODE == kModeMV) {
-              p.out[e] = o;
+              p.out[kofs + gi] = o;
             } else if (MODE == kModeMVR) {
-              if (p.v_norm_out) p.v_norm_out[e] = cur;
+              if (p.v_norm_out) p.v_norm_out[kofs + gi] = cur;
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
-              if (k == 0) {
-                p.vh[gi] = sval;
-              } else {
-                const int pos = (k - 1) % p.nu;
-                acc[r] = (pos == 0) ? sval : __dadd_rn(acc[r], sval);
-                if (pos == p.nu - 1) p.vh[(int64_t)((k - 1) / p.nu + 1) * m + gi] = acc[r];
-              }
+              acc[r] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[r], sval);
+              if (pos == nu - 1) p.vh[(int64_t)K * m + gi] = acc[r];
             } else {
-              if (p.x_out) p.x_out[e] = cur;
-              if (p.out) p.out[e] = o;
+              if (p.x_out) p.x_out[kofs + gi] = cur;
+              if (p.out) p.out[kofs + gi] = o;
               if (p.partials) {
-                double z = v0v[r];
-                if (p.v0_scale) z = __ddiv_rn(z, v0sc);
-                dot = __dadd_rn(dot, __dmul_rn(o, z));
+                dot = __dadd_rn(dot, __dmul_rn(o, v0v[r]));
               }
             }
           }
@@ -342,13 +345,13 @@ bool encode_1d(CUtensorMap *map, const double *base, int64_t n) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER>
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED>
 int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
             int *n_partials, double bytes, int cat) {
   constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
   constexpr int ROWS = (DIM == 2) ? R + 2 : 1;
   const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
-  auto kern = march_tma_kernel<MODE, DIM, R, S, VAR, GATHER>;
+  auto kern = march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED>;
   static int occ = -1;
   if (occ < 0) {
     PMK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -406,39 +409,38 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
   } else {
     mvt = mv;
   }
+  if (mode == kModeIMV && p.v0_scale) return 0;  // lazily scaled v_0: register path
   const bool var = p.P.var || p.Q.var;
   const bool d2 = p.ny > 1;
+  const bool scaled = p.v_scale != nullptr;
   int rc = 0;
-#define PMK_RUN(MODE, DIM, R, S, VAR, GATHER) \
-  rc = run_tma<MODE, DIM, R, S, VAR, GATHER>(p, mv, mvt, s, n_partials, bytes, cat)
+  // R = 8 rows per tile in 2-D; S-stage rings sized for 2-3 CTAs per SM
+#define PMK_RUN(MODE, DIM, R, S, GATHER)                                                        \
+  do {                                                                                         \
+    if (var) {                                                                                 \
+      rc = scaled ? run_tma<MODE, DIM, R, S, true, GATHER, true>(p, mv, mvt, s, n_partials,     \
+                                                                 bytes, cat)                   \
+                  : run_tma<MODE, DIM, R, S, true, GATHER, false>(p, mv, mvt, s, n_partials,    \
+                                                                  bytes, cat);                 \
+    } else {                                                                                   \
+      rc = scaled ? run_tma<MODE, DIM, R, S, false, GATHER, true>(p, mv, mvt, s, n_partials,    \
+                                                                  bytes, cat)                  \
+                  : run_tma<MODE, DIM, R, S, false, GATHER, false>(p, mv, mvt, s, n_partials,   \
+                                                                   bytes, cat);                \
+    }                                                                                          \
+  } while (0)
   switch (mode) {
     case kModeMV:
-      if (d2) {
-        if (var) PMK_RUN(kModeMV, 2, 8, 3, true, false); else PMK_RUN(kModeMV, 2, 8, 3, false, false);
-      } else {
-        if (var) PMK_RUN(kModeMV, 1, 1, 8, true, false); else PMK_RUN(kModeMV, 1, 1, 8, false, false);
-      }
+      if (d2) PMK_RUN(kModeMV, 2, 8, 3, false); else PMK_RUN(kModeMV, 1, 1, 8, false);
       break;
     case kModeMVR:
-      if (d2) {
-        if (var) PMK_RUN(kModeMVR, 2, 8, 3, true, false); else PMK_RUN(kModeMVR, 2, 8, 3, false, false);
-      } else {
-        if (var) PMK_RUN(kModeMVR, 1, 1, 8, true, false); else PMK_RUN(kModeMVR, 1, 1, 8, false, false);
-      }
+      if (d2) PMK_RUN(kModeMVR, 2, 8, 3, false); else PMK_RUN(kModeMVR, 1, 1, 8, false);
       break;
     case kModeIMV:
       if (d2) {
-        if (gather) {
-          if (var) PMK_RUN(kModeIMV, 2, 8, 3, true, true); else PMK_RUN(kModeIMV, 2, 8, 3, false, true);
-        } else {
-          if (var) PMK_RUN(kModeIMV, 2, 8, 2, true, false); else PMK_RUN(kModeIMV, 2, 8, 2, false, false);
-        }
+        if (gather) PMK_RUN(kModeIMV, 2, 8, 3, true); else PMK_RUN(kModeIMV, 2, 8, 2, false);
       } else {
-        if (gather) {
-          if (var) PMK_RUN(kModeIMV, 1, 1, 8, true, true); else PMK_RUN(kModeIMV, 1, 1, 8, false, true);
-        } else {
-          if (var) PMK_RUN(kModeIMV, 1, 1, 8, true, false); else PMK_RUN(kModeIMV, 1, 1, 8, false, false);
-        }
+        if (gather) PMK_RUN(kModeIMV, 1, 1, 8, true); else PMK_RUN(kModeIMV, 1, 1, 8, false);
       }
       break;
     default:

@@ -384,15 +384,22 @@ def _state(hier, level_idx, want_arrays=False):
     return out
 
 
-def _check_memory(nbytes: int) -> None:
-    import torch
+class _MemoryBudget:
+    """Device bytes still available for Krylov vectors (one cudaMemGetInfo
+    per fgmres call; per-iteration checks are host arithmetic only)."""
 
-    free, _total = torch.cuda.mem_get_info()
-    reserve = torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
-    if nbytes > free + reserve - (256 << 20):
-        raise MemoryError(
-            f"FGMRES basis needs {nbytes / 2**30:.1f} GiB more device memory than is free; "
-            "set SolverConfig.restart to bound the basis")
+    def __init__(self):
+        import torch
+
+        free, _total = torch.cuda.mem_get_info()
+        cached = torch.cuda.memory_reserved() - torch.cuda.memory_allocated()
+        self.left = free + cached - (512 << 20)
+
+    def take(self, nbytes: int) -> None:
+        self.left -= nbytes
+        if self.left < 0:
+            raise MemoryError(
+                "FGMRES basis exceeds free device memory; set SolverConfig.restart to bound it")
 
 
 def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_iter: int,
@@ -421,10 +428,11 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
         return torch.zeros_like(b), report
     vs, cos = [], []
     per_iter = 8 * (lvl.total_dim + nxt.total_dim)
-    _check_memory(8 * lvl.total_dim)
+    budget = _MemoryBudget()
+    budget.take(8 * lvl.total_dim)
     w = _empty(lvl.total_dim)  # unnormalised new vector, reused every iteration
     for j in range(max_iter):
-        _check_memory(per_iter)
+        budget.take(per_iter)
         v = _empty(lvl.total_dim)
         co = _empty(nxt.total_dim)
         vs.append(v)
