@@ -114,6 +114,14 @@ typedef struct pmk_coarse {
   const double *dinv;     /* DENSE: [m][m] */
   pmk_stencil coupling;   /* DENSE: C as a stencil in row form */
   double *work0, *work1;  /* device scratch, (n_steps+1)*m doubles each */
+  /* DST via FFT (n+1 a power of two): per direction [N] complex four-step
+   * twiddles w_N^{n2 k1} at [k1*N2 + n2] (N2 = 2^floor(log2 N / 2)) followed
+   * by [N] complex (cos, sin)(pi p/N) (pmk_dst.cu); NULL selects
+   * the dense sine-matrix GEMM path (sx/sy).  With the FFT path delta/beta
+   * are ordered x-mode slow, y-mode fast, and fft_scale (= 4/(N_x N_y), or
+   * 2/N_x in 1-D) folds the orthonormalisation into the recurrence. */
+  const double *fft_x, *fft_y;
+  double fft_scale;
 } pmk_coarse;
 
 /* ---------------------------------------------------------------- per-op */

@@ -18,7 +18,7 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _lib
-from .spatial import dst_eigenvalues_1d, dst_matrix
+from .spatial import dst_eigenvalues_1d, dst_matrix, fft_dst_tables
 
 # Largest spatial size for which the DENSE coarsest solve is allowed
 # (explicit inverse of m*m doubles: 8192^2 * 8 B = 512 MB).
@@ -132,12 +132,28 @@ class CoarseSolver:
         if spectral is not None:
             d.kind = _lib.PMK_COARSE_DST
             ex = dst_eigenvalues_1d(self.nx)
+            tabx = fft_dst_tables(self.nx)
+            taby = fft_dst_tables(self.ny) if self.ny > 1 else None
+            use_fft = (tabx is not None and self.nx + 1 <= 1024
+                       and (self.ny == 1 or (taby is not None and self.ny + 1 <= 512)))
             if self.ny > 1:
                 ey = dst_eigenvalues_1d(self.ny)
-                lam = spectral.factor * (ey[:, None] + ex[None, :])
+                lam = spectral.factor * (ey[:, None] + ex[None, :])  # y-mode slow
             else:
                 lam = spectral.factor * ex[None, :]
             lam = lam.ravel()
+            self.kind_detail = "dst-fft" if use_fft else "dst-gemm"
+            if use_fft:
+                fx = torch.from_numpy(tabx).cuda()
+                self._keep.append(fx)
+                d.fft_x = fx.data_ptr()
+                scale = 2.0 / (self.nx + 1)
+                if self.ny > 1:
+                    fy = torch.from_numpy(taby).cuda()
+                    self._keep.append(fy)
+                    d.fft_y = fy.data_ptr()
+                    scale *= 2.0 / (self.ny + 1)
+                d.fft_scale = scale
             delta = 1.0 - spectral.a_dt * lam
             beta = 1.0 + spectral.b_dt * lam
             sx = torch.from_numpy(dst_matrix(self.nx)).cuda()

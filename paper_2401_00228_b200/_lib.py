@@ -46,7 +46,8 @@ class CoarseDesc(ctypes.Structure):
                 ("n_steps", c_int32), ("dropped", c_void_p), ("sx", c_void_p),
                 ("sy", c_void_p), ("delta", c_void_p), ("beta", c_void_p),
                 ("dinv", c_void_p), ("coupling", Stencil), ("work0", c_void_p),
-                ("work1", c_void_p)]
+                ("work1", c_void_p), ("fft_x", c_void_p), ("fft_y", c_void_p),
+                ("fft_scale", c_double)]
 
 
 # name -> (restype, argtypes); exactly the functions include/pintmk_b200.h declares

@@ -120,14 +120,16 @@ int gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double
 constexpr int kRecBatch = 8;
 __global__ void __launch_bounds__(256)
     dst_recurrence_kernel(double *X, const double *delta, const double *beta,
-                          const uint8_t *dropped, int n_steps, int m, const int *live) {
+                          const uint8_t *dropped, int n_steps, int m, double scale,
+                          const int *live) {
   if (!is_live(live)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   // multiply by 1/delta: high modes decay through the subnormal range, where
   // an IEEE division takes the slow path
   const double d = 1.0 / delta[i], b = beta[i];
-  double u = X[i];  // transformed rhs_0 == transformed out_0
+  double u = X[i] * scale;  // transformed rhs_0 == transformed out_0
+  X[i] = u;
   for (int k0 = 1; k0 <= n_steps; k0 += kRecBatch) {
     double r[kRecBatch];
 #pragma unroll
@@ -140,7 +142,8 @@ __global__ void __launch_bounds__(256)
       const int k = k0 + q;
       if (k > n_steps) break;
       const bool cut = dropped && dropped[k];
-      u = cut ? r[q] * d : fma(b, u, r[q]) * d;
+      const double rq = r[q] * scale;
+      u = cut ? rq * d : fma(b, u, rq) * d;
       X[(int64_t)k * m + i] = u;
     }
   }
@@ -211,6 +214,48 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
   const int m = nx * ny;
   const int rows = C.n_steps + 1;
   const int64_t N = (int64_t)rows * m;
+  if (C.kind == PMK_COARSE_DST && C.fft_x) {
+    // FFT sine transforms (pmk_dst.cu): every pass streams the vector once.
+    PMK_RETURN_IF(!C.delta || !C.beta || !C.work0, PMK_ERR_ARG);
+    int rc;
+    if (ny == 1) {
+      rc = launch_dst_rows(rhs, C.work0, nx, rows, C.fft_x, live, s);
+      if (rc) return rc;
+      {
+        prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
+        dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta,
+                                                             C.dropped, C.n_steps, m,
+                                                             C.fft_scale, live);
+      }
+      PMK_LAUNCH_CHECK();
+      rc = launch_dst_rows(C.work0, out, nx, rows, C.fft_x, live, s);
+      if (rc) return rc;
+    } else {
+      PMK_RETURN_IF(!C.fft_y || !C.work1, PMK_ERR_ARG);
+      // x then y (modes [k][q][p], q slow), recurrence, y then x
+      rc = launch_dst_rows(rhs, C.work0, nx, (int64_t)rows * ny, C.fft_x, live, s);
+      if (rc) return rc;
+      rc = launch_dst_cols(C.work0, C.work1, nx, ny, rows, C.fft_y, live, s);
+      if (rc) return rc;
+      {
+        prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
+        dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta,
+                                                             C.dropped, C.n_steps, m,
+                                                             C.fft_scale, live);
+      }
+      PMK_LAUNCH_CHECK();
+      rc = launch_dst_cols(C.work1, C.work0, nx, ny, rows, C.fft_y, live, s);
+      if (rc) return rc;
+      rc = launch_dst_rows(C.work0, out, nx, (int64_t)rows * ny, C.fft_x, live, s);
+      if (rc) return rc;
+    }
+    {
+      prof::Scope cs(prof::kCoarseMisc, 16.0 * m, 0.0, s);
+      copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);  // stepper.py:118
+    }
+    PMK_LAUNCH_CHECK();
+    return 0;
+  }
   if (C.kind == PMK_COARSE_DST) {
     PMK_RETURN_IF(!C.sx || !C.delta || !C.beta || !C.work0, PMK_ERR_ARG);
     if (ny == 1) {
@@ -219,7 +264,7 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       {
         prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
         dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta,
-                                                             C.dropped, C.n_steps, m, live);
+                                                             C.dropped, C.n_steps, m, 1.0, live);
       }
       PMK_LAUNCH_CHECK();
       rc = gemm(rows, nx, nx, C.work0, nx, 0, C.sx, nx, 0, out, nx, 0, 1, live, s);
@@ -235,7 +280,7 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       {
         prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
         dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta,
-                                                             C.dropped, C.n_steps, m, live);
+                                                             C.dropped, C.n_steps, m, 1.0, live);
       }
       PMK_LAUNCH_CHECK();
       rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work1, nx, m, C.work0, nx, m, rows, live, s);

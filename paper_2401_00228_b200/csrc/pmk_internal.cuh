@@ -161,6 +161,10 @@ int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_s
                             cudaStream_t s);
 
 // ---------------------------------------------------------------- coarse
+int launch_dst_rows(const double *in, double *out, int n, int64_t rows, const double *tables,
+                    const int *live, cudaStream_t s);
+int launch_dst_cols(const double *in, double *out, int nx, int ny, int slices,
+                    const double *tables, const int *live, cudaStream_t s);
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
                  cudaStream_t s);
 
