@@ -248,6 +248,11 @@ int pmk_profile_end(double *stats, int32_t max_categories,
 const char *pmk_profile_category(int32_t idx);
 int64_t pmk_launch_count(void);
 
+/* Diagnostics: out[i] = x[i] / d through the kernels' reciprocal-based
+ * correctly rounded division (must equal IEEE x / d bitwise). */
+int pmk_div_check(const double *x, double d, int64_t n, double *out,
+                  pmk_stream_t stream);
+
 /* Library identification (for the loaded-.so checks). */
 const char *pmk_version(void);
 

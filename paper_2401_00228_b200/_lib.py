@@ -86,6 +86,7 @@ SIGNATURES = {
     "pmk_profile_end": (c_int32, [POINTER(c_double), c_int32, POINTER(c_int32)]),
     "pmk_profile_category": (ctypes.c_char_p, [c_int32]),
     "pmk_launch_count": (c_int64, []),
+    "pmk_div_check": (c_int32, [c_void_p, c_double, c_int64, c_void_p, c_void_p]),
 }
 
 _lib = None

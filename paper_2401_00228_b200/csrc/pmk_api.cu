@@ -387,6 +387,11 @@ const char *pmk_version(void) { return "pintmk_b200 0.1 sm_100a"; }
 
 int64_t pmk_launch_count(void) { return g_launches.load(); }
 
+int pmk_div_check(const double *x, double d, int64_t n, double *out, pmk_stream_t stream) {
+  PMK_RETURN_IF(!x || !out || n < 0, PMK_ERR_ARG);
+  return launch_div_check(x, d, n, out, cs(stream));
+}
+
 int pmk_profile_begin(int32_t with_events) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   g_recs.clear();

@@ -57,6 +57,27 @@ __device__ __forceinline__ bool is_live(const int *live) {
   return live == nullptr || *live != 0;
 }
 
+// x / d, correctly rounded (bitwise __ddiv_rn), for a divisor d reused over
+// many x: y = RN(1/d) is computed once (`rcp`).  q0 = RN(x y) is within two
+// ulps; one FMA correction q1 = RN(q0 + (x - d q0) y) is faithful (its error
+// is |eps (x/d - q0)| + 1/2 ulp with |eps| <= 2^-53); Markstein's theorem
+// then makes q2 = RN(q1 + (x - d q1) y) the correctly rounded quotient (the
+// residuals are exact FMAs).  With d in [2^-100, 2^100] (div_ok) and |x| in
+// [2^-800, 2^800] the quotient and the residuals stay normal; other x (and
+// zeros) take the IEEE division.  Checked bitwise against IEEE division by
+// tests/test_gpu_parity.py (pmk_div_check).
+__device__ __forceinline__ double div_by(double x, double d, double rcp) {
+  const unsigned ex = (unsigned)(__double2hiint(x) >> 20) & 0x7ffu;
+  if (ex < 1023u - 800u || ex > 1023u + 800u) return x == 0.0 ? x : __ddiv_rn(x, d);
+  const double q0 = __dmul_rn(x, rcp);
+  const double q1 = __fma_rn(__fma_rn(-d, q0, x), rcp, q0);
+  return __fma_rn(__fma_rn(-d, q1, x), rcp, q1);
+}
+// Divisor usable by div_by (normal, not near the exponent limits).
+__host__ __device__ __forceinline__ bool div_ok(double d) {
+  return d >= 0x1p-100 && d <= 0x1p100;
+}
+
 // Deterministic block reduction: warp xor-tree, then warp 0 over the warp
 // sums.  Every block running this on the same inputs gets the same bits.
 // blockDim.x must be a multiple of 32 (<= 1024).
@@ -157,6 +178,7 @@ int launch_dot_partials(const double *a, const double *a_scale, const double *b,
                         const int *live, cudaStream_t s);
 int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *partials,
                            cudaStream_t s);
+int launch_div_check(const double *x, double d, int64_t n, double *out, cudaStream_t s);
 int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_sqrt,
                             cudaStream_t s);
 

@@ -337,6 +337,13 @@ __global__ void interpolate_kernel(const double *w, double *out, int nu, int n_T
   }
 }
 
+__global__ void div_check_kernel(const double *x, double d, int64_t n, double *out) {
+  const double rcp = __drcp_rn(d);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = div_by(x[i], d, rcp);
+}
+
 int grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
   if (g > 16 * kSMs) g = 16 * kSMs;
@@ -429,6 +436,13 @@ int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t 
   dim3 grid((m + 255) / 256, rows < 1024 ? rows : 1024);
   if (grid.x > 64) grid.x = 64;
   assemble_kernel<<<grid, 256, 0, s>>>(st, a, x, rows, m, nu, m_coarse, group_of, first);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+int launch_div_check(const double *x, double d, int64_t n, double *out, cudaStream_t s) {
+  if (!div_ok(d)) return PMK_ERR_ARG;
+  div_check_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, d, n, out);
   PMK_LAUNCH_CHECK();
   return 0;
 }

@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   // TMA tensor destinations must be 128-byte aligned; dynamic shared memory
   // follows the static part at an unspecified alignment, so align by hand.
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  // (offset arithmetic on the shared pointer keeps shared-space loads)
   double *smem = reinterpret_cast<double *>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~static_cast<uintptr_t>(127));
+      smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
   __shared__ __align__(8) uint64_t bars[S];
 
   if (!is_live(p.live)) return;
@@ -128,6 +129,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int tiles = g.gx * g.gy;
   const int64_t n_items = (int64_t)tiles * g.n_chunks;
   const double vsc = SCALED ? *p.v_scale : 1.0;
+  const bool fastdiv = SCALED && div_ok(vsc);
+  const double vrcp = fastdiv ? __drcp_rn(vsc) : 1.0;
   double dot = 0.0;
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           double u = *cell;
           // 0 / scale = 0 (scale > 0): skipping it keeps exact zeros (the
           // first Krylov vector is mostly zero) off the division slow path
-          if (SCALED && u != 0.0) u = __ddiv_rn(u, vsc);
+          if (SCALED && u != 0.0) u = fastdiv ? div_by(u, vsc, vrcp) : __ddiv_rn(u, vsc);
           if (MODE == kModeIMV) {
             const double z = GATHER ? __ldg(vtk + p.group_of[y * nx + px])
                                     : sv[(ROWS + r) * kBox + t + ((pK + (y & nx)) & 1)];
@@ -429,16 +432,42 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
                                                                    bytes, cat);                \
     }                                                                                          \
   } while (0)
+  // tile rows x ring stages per mode (tuning knob PMK_TMA_CFG=<mvr>,<imv>,
+  // each one of 0: 8x3/8x2, 1: 8x4/4x3, 2: 4x4/4x4, 3: 16x2/8x3)
+  static int cfg_mvr = -1, cfg_imv = -1;
+  if (cfg_mvr < 0) {
+    cfg_mvr = 0;
+    cfg_imv = 0;
+    if (const char *e = getenv("PMK_TMA_CFG")) sscanf(e, "%d,%d", &cfg_mvr, &cfg_imv);
+  }
   switch (mode) {
     case kModeMV:
       if (d2) PMK_RUN(kModeMV, 2, 8, 3, false); else PMK_RUN(kModeMV, 1, 1, 8, false);
       break;
     case kModeMVR:
-      if (d2) PMK_RUN(kModeMVR, 2, 8, 3, false); else PMK_RUN(kModeMVR, 1, 1, 8, false);
+      if (d2) {
+        switch (cfg_mvr) {
+          case 1: PMK_RUN(kModeMVR, 2, 8, 4, false); break;
+          case 2: PMK_RUN(kModeMVR, 2, 4, 4, false); break;
+          case 3: PMK_RUN(kModeMVR, 2, 16, 2, false); break;
+          default: PMK_RUN(kModeMVR, 2, 8, 3, false);
+        }
+      } else {
+        PMK_RUN(kModeMVR, 1, 1, 8, false);
+      }
       break;
     case kModeIMV:
       if (d2) {
-        if (gather) PMK_RUN(kModeIMV, 2, 8, 3, true); else PMK_RUN(kModeIMV, 2, 8, 2, false);
+        if (gather) {
+          PMK_RUN(kModeIMV, 2, 8, 3, true);
+        } else {
+          switch (cfg_imv) {
+            case 1: PMK_RUN(kModeIMV, 2, 4, 3, false); break;
+            case 2: PMK_RUN(kModeIMV, 2, 4, 4, false); break;
+            case 3: PMK_RUN(kModeIMV, 2, 8, 3, false); break;
+            default: PMK_RUN(kModeIMV, 2, 8, 2, false);
+          }
+        }
       } else {
         if (gather) PMK_RUN(kModeIMV, 1, 1, 8, true); else PMK_RUN(kModeIMV, 1, 1, 8, false);
       }

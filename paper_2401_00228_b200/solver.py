@@ -454,7 +454,7 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
     if keep_basis:
         basis = [vs[l].cpu().numpy() for l in range(n_iter)]
         if not st["breakdown"]:
-            basis.append((w / st["hraw"][n_iter, n_iter - 1]).cpu().numpy())
+            basis.append(w.cpu().numpy() / st["hraw"][n_iter, n_iter - 1])  # IEEE division
         pre = [(vs[l] - lvl.pair.interpolate(cos[l])).cpu().numpy() for l in range(n_iter)]
         report.metadata["basis"] = basis
         report.metadata["preconditioned"] = pre
