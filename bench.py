@@ -55,10 +55,9 @@ def parse():
 
 
 def dist_info():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    from paper_2401_00228_b200.dist import rank_info
+
+    return rank_info()
 
 
 def peaks():
@@ -172,13 +171,16 @@ def run_ours(args):
     from paper_2401_00228_b200 import _lib, multilevel_solve
     from tests.cases import BASELINE, gpu_hierarchy
 
+    from paper_2401_00228_b200 import dist as pdist
+
     rank, world, local = dist_info()
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
-    case = BASELINE[args.case].scaled(seed=BASELINE[args.case].seed + rank)
+        pdist.init("nccl")
+    # replicas: every rank solves its own seeded instance (no data-path collective)
+    case = BASELINE[args.case].scaled(seed=pdist.instance_seed(BASELINE[args.case].seed, rank))
     u0 = torch.from_numpy(case.u0_vector()).cuda()
     hier = gpu_hierarchy(case, u0=u0)
 
@@ -186,8 +188,7 @@ def run_ours(args):
         x, rep = multilevel_solve(hier)
         del x
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    pdist.barrier()
     torch.cuda.synchronize()
 
     sampler = ClockSampler(local)
@@ -210,12 +211,8 @@ def run_ours(args):
     launches = _lib.launch_count() - n0
     kernels = _lib.profile_end() if profile else {}
     clocks = sampler.stop()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        dist.barrier()
+    ms = pdist.max_over_ranks(ev0.elapsed_time(ev1), device="cuda")
+    pdist.barrier()
     ms_per_step = ms / args.steps
     value = case.N * args.steps * world / (ms / 1000.0)
 
@@ -227,8 +224,7 @@ def run_ours(args):
     e2e_t = []
     for _ in range(max(args.e2e_steps, 0)):
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
+        pdist.barrier()
         t0 = time.perf_counter()
         h2 = gpu_hierarchy(case, u0=pin_u0)
         xh, rep2 = multilevel_solve(h2, out=pin_x)
@@ -236,11 +232,7 @@ def run_ours(args):
         e2e_t.append(time.perf_counter() - t0)
         del h2, xh
         torch.cuda.empty_cache()
-    e2e_s = max(e2e_t) if e2e_t else float("nan")
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = pdist.max_over_ranks(max(e2e_t), device="cuda") if e2e_t else float("nan")
 
     # ----- roofline of the dominant memory-bound kernel
     peak, peak_kind = peaks()
