@@ -197,6 +197,15 @@ __global__ void __launch_bounds__(kTmaThreads)
     const int nu = p.nu;
     const int xo = x - boxx;         // box offset of this thread's output column
     const int gx0 = y0 * nx + x;     // in-slice index of (y0, x)
+    double v0next[RO];
+    if (MODE == kModeIMV && p.partials) {
+      const int kf = (kb > kstart) ? kb : kstart;  // first non-prime slice
+#pragma unroll
+      for (int r = 0; r < RO; ++r)
+        v0next[r] = (xin && kf < ke && y0 + r < ny)
+                        ? __ldg(p.v0 + (int64_t)kf * m + gx0 + r * nx)
+                        : 0.0;
+    }
     for (int i = 0; i < nsl; ++i, ++it) {
       // ---- per-slice uniform quantities
       const int k = kstart + i;
@@ -209,12 +218,17 @@ __global__ void __launch_bounds__(kTmaThreads)
       const int pk = (int)(((int64_t)k * m + boxx) & 1);  // row parity shifts (issue())
       const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
       const int64_t kofs = (int64_t)k * m;
-      // IMV: start the v_0 loads of the dot early
+      // IMV: v_0 of this slice (prefetched one slice ahead) for the dot
       double v0v[RO];
-      if (MODE == kModeIMV && p.partials && !prime && xin) {
-        const double *v0k = p.v0 + kofs + gx0;
+      if (MODE == kModeIMV && p.partials) {
 #pragma unroll
-        for (int r = 0; r < RO; ++r) v0v[r] = (y0 + r < ny) ? __ldg(v0k + r * nx) : 0.0;
+        for (int r = 0; r < RO; ++r) v0v[r] = v0next[r];
+        const int kn = k + 1;  // prefetch the next slice of this item
+        if (kn < ke && xin) {
+          const double *v0k = p.v0 + (int64_t)kn * m + gx0;
+#pragma unroll
+          for (int r = 0; r < RO; ++r) v0next[r] = (y0 + r < ny) ? __ldg(v0k + r * nx) : 0.0;
+        }
       }
       mbar_wait(&bars[stage], (it / S) & 1);
       // ---- pre-pass: u = v / scale  or  u = v - Z vt, once per element
@@ -248,7 +262,7 @@ __global__ void __launch_bounds__(kTmaThreads)
 #pragma unroll
         for (int r = 0; r < RO; ++r) {
           const int y = y0 + r;
-          if (DIM == 2 && y >= ny) break;
+          const bool rv = DIM == 1 || y < ny;  // row exists (last tile may be partial)
           const double *row = col + ((DIM == 2) ? (r + 1) * kBox : 0) + ((pk + (y & nx)) & 1);
           const double dn = (DIM == 2 && y < ny - 1)
                                 ? col[(r + 2) * kBox + ((pk + ((y + 1) & nx)) & 1)]
@@ -274,7 +288,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           Qu = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(Qu, __dmul_rn(b.w, lf)), __dmul_rn(b.c, cur)),
                                    __dmul_rn(b.e, rt)),
                          __dmul_rn(b.n, dn));
-          if (!prime) {
+          if (!prime && rv) {
             double o;
             if (k == 0) {
               o = cur;  // identity block row (stepper.py:100)

@@ -11,7 +11,7 @@ import sys
 
 
 def short_name(name: str) -> str:
-    m = re.search(r"march_tma_kernel<\(int\)(\d), \(int\)(\d)", name)
+    m = re.search(r"march_tma_kernel<(?:\(int\))?(\d), (?:\(int\))?(\d)", name)
     if m:
         return {"0": "march_mv", "1": "march_mvr", "2": "march_imv"}[m.group(1)] + f"[{m.group(2)}d]"
     base = re.sub(r"\(.*", "", name)
