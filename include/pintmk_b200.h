@@ -89,6 +89,20 @@ typedef struct pmk_pair {
   const int32_t *y_ptr;    /* device [m_coarse+1] */
   const int32_t *y_idx;    /* device [nnz] fine indices, ascending per row */
   const double *y_val;     /* device [nnz] Y entries (1/|group|) */
+  /* MgritPair (intergrid.py:134-167), mgrit != 0: restriction injects every
+   * nu-th row; interpolation sets out[nu K] = w[K] and propagates
+   * out[nu K + j] = (psi^{-1} phi)^j w[K], j < nu, which is diagonal in the
+   * sine basis of the (pristine) fine level: ratio[mode] = beta / delta.
+   * Sine tables as in pmk_coarse (fft_* non-NULL: FFT path with fft_scale,
+   * else the dense sx/sy GEMM path).  Scratch: work0/work1/work2 of
+   * n_T*m_fine doubles, coarse_out of (n_T+1)*m_fine (the coarse solve's
+   * output inside the preconditioner). */
+  int32_t mgrit;
+  int32_t dim, nx, ny;
+  const double *sx, *sy, *fft_x, *fft_y;
+  double fft_scale;
+  const double *ratio;
+  double *work0, *work1, *work2, *coarse_out;
 } pmk_pair;
 
 /*
@@ -204,7 +218,7 @@ int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs,
  * normalised basis vector v_j into v_out (rhs/beta for j = 0, else the
  * previous step's w / h[j][j-1]); the unnormalised next vector goes to w_next
  * (may be the previous step's w_next, never the rhs) and the child solve to
- * child_out.  tol > 0 stops the device-side iteration once rel <= tol
+ * child_out (for an MGRIT pair: its interpolation, fine-level size).  tol > 0 stops the device-side iteration once rel <= tol
  * (solver.py:438); tol = 0 is the reference's tol=None.  finish: back substitution
  * and x = sum_i y_i x_i with x_i = v_i - Z vt_i recomputed (no stored
  * preconditioned vectors). */
@@ -230,7 +244,8 @@ int pmk_fgmres_fixed(pmk_hier *H, int32_t idx, double *x,
 
 /* apply_preconditioner (solver.py:323-359) at level idx < n_levels-1:
  * out = v - Z A_H^{-1} Y^T (A v - mu v).  Uses the registered buffers of
- * level idx+1 and child_out as the coarse-correction buffer. */
+ * level idx+1 and child_out as the coarse-correction buffer (fine-level size
+ * for an MGRIT pair). */
 int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v,
                              double *child_out, double *out,
                              pmk_stream_t stream);

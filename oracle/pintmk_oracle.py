@@ -217,8 +217,9 @@ def agglomerate(nx: int, ny: int = 1):
 
 @dataclass(eq=False)
 class Pair:
-    """TimePair (intergrid.py:37-63) when groups is None, else TimeSpacePair
-    (intergrid.py:79-120)."""
+    """TimePair (intergrid.py:37-63) when groups is None, TimeSpacePair
+    (intergrid.py:79-120) with groups, MgritPair (intergrid.py:134-167) when
+    `phi` is set (coarse-point injection, ideal interpolation)."""
 
     nu: int
     n_T: int
@@ -226,6 +227,8 @@ class Pair:
     groups: list | None = None
     y: sp.csr_matrix | None = None
     z: sp.csr_matrix | None = None
+    phi: sp.csr_matrix | None = None     # MGRIT: fine phi
+    psi_solve: object | None = None      # MGRIT: fine psi factorisation
 
     @property
     def m(self) -> int:
@@ -242,8 +245,11 @@ def make_ts_pair(nu, n_T, groups, n) -> Pair:
 
 
 def restrict(p: Pair, v: np.ndarray) -> np.ndarray:
-    """intergrid.py:51-56 / 106-112."""
+    """intergrid.py:51-56 / 106-112 / 152-155 (MGRIT injection)."""
     blk = np.ascontiguousarray(v).reshape(p.nu * p.n_T + 1, -1)
+    if p.phi is not None:
+        out = blk[::p.nu].copy()
+        return out.reshape(-1) if v.ndim == 1 else out
     summed = blk[1:].reshape(p.n_T, p.nu, p.n).sum(axis=1)
     out = np.empty((p.n_T + 1, p.m))
     if p.groups is None:
@@ -256,8 +262,17 @@ def restrict(p: Pair, v: np.ndarray) -> np.ndarray:
 
 
 def interpolate(p: Pair, w: np.ndarray) -> np.ndarray:
-    """intergrid.py:58-63 / 114-120."""
+    """intergrid.py:58-63 / 114-120 / 157-167 (MGRIT: propagate each coarse
+    row through the nu - 1 fine steps with zero forcing)."""
     blk = np.ascontiguousarray(w).reshape(p.n_T + 1, -1)
+    if p.phi is not None:
+        out = np.zeros((p.nu * p.n_T + 1, p.n))
+        out[::p.nu] = blk
+        cur = blk[:-1]
+        for j in range(1, p.nu):
+            cur = np.ascontiguousarray(p.psi_solve((cur @ p.phi).T).T)
+            out[j::p.nu] = cur
+        return out.reshape(-1) if w.ndim == 1 else out
     if p.groups is not None:
         blk = blk @ p.z.T
     out = np.empty((p.nu * p.n_T + 1, p.n))
@@ -364,6 +379,27 @@ def budgets_for(n_inter: int, inner_iters) -> list:
     if len(out) != n_inter:
         raise ValueError("need one inner budget per intermediate level")
     return out
+
+
+def build_mgrit(dim, nx, ny, theta, dt, n_t, u0, cfg: Config, nu=2, tau=1.0,
+                length=1.0) -> Hierarchy:
+    """build_two_level(fine, "MGRIT", nu, cfg) (solver.py:248-265): MgritPair
+    (intergrid.py:134-167) + rediscretized coarse system (intergrid.py:270-280)."""
+    a, _dx = laplacian(dim, nx, ny, tau, length)
+    d, b = blocks_from(a, theta, dt)
+    fine = System(d, b, n_t)
+    rhs = np.zeros((n_t + 1, a.shape[0]))
+    rhs[0] = u0
+    if n_t % nu:
+        raise ValueError("nu must divide n_t")
+    n_T = n_t // nu
+    top = Rung(fine, a, dt, theta, n_t, (nx, ny if dim == 2 else 1), dim, "fine")
+    top.pair = Pair(nu, n_T, a.shape[0], phi=b, psi_solve=fine.solver())
+    dc, bc = blocks_from(a, theta, nu * dt)
+    coarse = Rung(System(dc, bc, n_T), a, nu * dt, theta, n_T, top.grid, dim, "mgrit")
+    if cfg.coarsest_n_cgs >= 1:
+        coarse.system = System(dc, bc, n_T, decouple(n_T, cfg.coarsest_n_cgs))
+    return Hierarchy([top, coarse], rhs, fine, cfg, ["MGRIT"])
 
 
 def build(dim, nx, ny, theta, dt, n_t, u0, n_levels, schedule, cfg: Config, nu=2,

@@ -38,7 +38,11 @@ class LevelDesc(ctypes.Structure):
 class PairDesc(ctypes.Structure):
     _fields_ = [("nu", c_int32), ("n_T", c_int32), ("m_fine", c_int32),
                 ("m_coarse", c_int32), ("group_of", c_void_p), ("y_ptr", c_void_p),
-                ("y_idx", c_void_p), ("y_val", c_void_p)]
+                ("y_idx", c_void_p), ("y_val", c_void_p), ("mgrit", c_int32),
+                ("dim", c_int32), ("nx", c_int32), ("ny", c_int32), ("sx", c_void_p),
+                ("sy", c_void_p), ("fft_x", c_void_p), ("fft_y", c_void_p),
+                ("fft_scale", c_double), ("ratio", c_void_p), ("work0", c_void_p),
+                ("work1", c_void_p), ("work2", c_void_p), ("coarse_out", c_void_p)]
 
 
 class CoarseDesc(ctypes.Structure):

@@ -142,6 +142,13 @@ int check_pair(const pmk_level &L, const pmk_pair *P) {
   PMK_RETURN_IF(P->nu < 1 || P->n_T < 0, PMK_ERR_ARG);
   PMK_RETURN_IF(P->nu * P->n_T != L.n_steps, PMK_ERR_SHAPE);
   PMK_RETURN_IF(P->m_fine != L.nx * L.ny, PMK_ERR_SHAPE);
+  if (P->mgrit) {
+    PMK_RETURN_IF(P->group_of || P->m_coarse != P->m_fine, PMK_ERR_SHAPE);
+    PMK_RETURN_IF(!P->ratio || !P->work0 || !P->work1 || !P->work2 || !P->coarse_out,
+                  PMK_ERR_ARG);
+    PMK_RETURN_IF(!P->fft_x && !P->sx, PMK_ERR_ARG);
+    return 0;
+  }
   const bool space = P->group_of != nullptr;
   PMK_RETURN_IF(space && (!P->y_ptr || !P->y_idx || !P->y_val), PMK_ERR_ARG);
   PMK_RETURN_IF(!space && P->m_coarse != P->m_fine, PMK_ERR_SHAPE);
@@ -173,6 +180,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   p.v_norm_out = v_norm_out;
   p.mu = mu;
   p.nu = P.nu;
+  p.inject = P.mgrit ? 1 : 0;  // MgritPair.restrict (intergrid.py:152-155)
   const bool space = P.group_of != nullptr;
   PMK_RETURN_IF(space && !scratch, PMK_ERR_ARG);
   p.vh = space ? scratch : vh;
@@ -183,17 +191,18 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   return 0;
 }
 
-// x = v - Z vt ; w = A x ; partial <w, v0>
+// x = v - Z vt ; w = A x ; partial <w, v0>.  For MGRIT pairs vt is the
+// already interpolated fine vector (identity coarse mapping).
 int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double *v_scale,
            const double *vt, double *x, double *w, const double *v0, const double *v0_scale,
            double *partials, int *n_partials, const int *live, cudaStream_t s) {
   MarchParams p = base_params(L);
   p.v = v;
   p.v_scale = v_scale;
-  p.nu = P.nu;
+  p.nu = P.mgrit ? 1 : P.nu;
   p.vt = vt;
   p.group_of = P.group_of;
-  p.m_coarse = P.m_coarse;
+  p.m_coarse = P.mgrit ? P.m_fine : P.m_coarse;
   p.x_out = x;
   p.out = w;
   p.v0 = v0;
@@ -300,7 +309,15 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   int rc = do_mvr(R.L, R.P, H->mu, R.pending, K.vscale + j, vh, R.ts_scratch, v_out, live, s);
   if (rc) return rc;
   R.v.push_back(v_out);
-  rc = child_solve(H, idx, child_out, live, s);
+  if (R.P.mgrit) {
+    // coarse solve into the pair's scratch, then ideal interpolation into the
+    // iteration's (fine-size) child_out (intergrid.py:157-167)
+    rc = child_solve(H, idx, R.P.coarse_out, live, s);
+    if (rc) return rc;
+    rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, live, s);
+  } else {
+    rc = child_solve(H, idx, child_out, live, s);
+  }
   if (rc) return rc;
   // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407)
   int np = 0;
@@ -345,7 +362,11 @@ int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
       a.vt[a.count] = R.vt[l];
       ++a.count;
     }
-    rc = launch_assemble(R.d_state, a, x, R.N, m, R.P.nu, R.P.m_coarse, R.P.group_of, first, s);
+    if (R.P.mgrit)  // vt_l are the interpolated fine vectors
+      rc = launch_assemble(R.d_state, a, x, R.N, m, 1, m, nullptr, first, s);
+    else
+      rc = launch_assemble(R.d_state, a, x, R.N, m, R.P.nu, R.P.m_coarse, R.P.group_of, first,
+                           s);
     if (rc) return rc;
     first += kAsmChunk;
   } while (first < n);
@@ -439,6 +460,7 @@ int pmk_stmv(const pmk_level *L, const double *v, double *out, pmk_stream_t stre
 int pmk_restrict(const pmk_pair *P, const double *v, double *vh, double *scratch,
                  pmk_stream_t stream) {
   PMK_RETURN_IF(!P || !v || !vh, PMK_ERR_ARG);
+  if (P->mgrit) return mgrit_restrict(*P, v, vh, nullptr, cs(stream));
   if (P->group_of) {
     PMK_RETURN_IF(!scratch, PMK_ERR_ARG);
     pmk_pair tp = *P;
@@ -451,6 +473,7 @@ int pmk_restrict(const pmk_pair *P, const double *v, double *vh, double *scratch
 
 int pmk_interpolate(const pmk_pair *P, const double *w, double *out, pmk_stream_t stream) {
   PMK_RETURN_IF(!P || !w || !out, PMK_ERR_ARG);
+  if (P->mgrit) return mgrit_interpolate(*P, w, out, nullptr, cs(stream));
   return launch_interpolate(*P, w, out, cs(stream));
 }
 
@@ -639,7 +662,13 @@ int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v, double *
   PMK_RETURN_IF(!vh, PMK_ERR_STATE);
   int rc = do_mvr(R.L, R.P, H->mu, v, nullptr, vh, R.ts_scratch, nullptr, nullptr, s);
   if (rc) return rc;
-  rc = child_solve(H, idx, child_out, nullptr, s);
+  if (R.P.mgrit) {
+    rc = child_solve(H, idx, R.P.coarse_out, nullptr, s);
+    if (rc) return rc;
+    rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, nullptr, s);
+  } else {
+    rc = child_solve(H, idx, child_out, nullptr, s);
+  }
   if (rc) return rc;
   // out = v - Z vt (the matvec output of the fused kernel is not needed)
   return do_imv(R.L, R.P, v, nullptr, child_out, out, nullptr, nullptr, nullptr, nullptr,

@@ -206,7 +206,111 @@ __global__ void gemv_kernel(const double *__restrict__ Dinv, const double *__res
   if (lane == 0) out[row] = acc;
 }
 
+// dst[K * dstride + doff + i] = src[K * sstride + soff + i], i < m, K < rows
+__global__ void strided_rows_copy_kernel(const double *src, int64_t sstride, int64_t soff,
+                                         double *dst, int64_t dstride, int64_t doff, int m,
+                                         int rows, const int *live) {
+  if (!is_live(live)) return;
+  for (int K = blockIdx.y; K < rows; K += gridDim.y)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+      dst[K * dstride + doff + i] = src[K * sstride + soff + i];
+}
+
+// work2[e] = scale * work1[e] * ratio[e % m]^j
+__global__ void mode_power_kernel(const double *w1, double *w2, const double *ratio, int m,
+                                  int64_t n, int j, double scale, const int *live) {
+  if (!is_live(live)) return;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double r = ratio[e % m];
+    double f = scale;
+    for (int q = 0; q < j; ++q) f *= r;
+    w2[e] = w1[e] * f;
+  }
+}
+
+int strided_copy(const double *src, int64_t sstride, int64_t soff, double *dst, int64_t dstride,
+                 int64_t doff, int m, int rows, const int *live, cudaStream_t s) {
+  dim3 grid((m + 255) / 256 < 64 ? (m + 255) / 256 : 64, rows < 4096 ? rows : 4096);
+  prof::Scope sc(prof::kXfer, 16.0 * m * (double)rows, 0.0, s);
+  strided_rows_copy_kernel<<<grid, 256, 0, s>>>(src, sstride, soff, dst, dstride, doff, m, rows,
+                                                live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
 }  // namespace
+
+// MgritPair.restrict (intergrid.py:152-155): vh[K] = v[nu K].
+int mgrit_restrict(const pmk_pair &P, const double *v, double *vh, const int *live,
+                   cudaStream_t s) {
+  const int64_t m = P.m_fine;
+  return strided_copy(v, (int64_t)P.nu * m, 0, vh, m, 0, (int)m, P.n_T + 1, live, s);
+}
+
+// MgritPair.interpolate (intergrid.py:157-167): out[nu K] = w[K]; rows
+// nu K + j (j < nu) = (psi^{-1} phi)^j w[K], applied as ratio^j in the sine
+// basis of the fine grid: one forward transform of w[0..n_T), then per j a
+// scaled copy and an inverse transform written into the strided rows.
+int mgrit_interpolate(const pmk_pair &P, const double *w, double *out, const int *live,
+                      cudaStream_t s) {
+  const int nx = P.nx, ny = (P.dim == 2) ? P.ny : 1;
+  const int m = nx * ny, nT = P.n_T, nu = P.nu;
+  const int64_t Nw = (int64_t)nT * m;
+  PMK_RETURN_IF(!P.ratio || !P.work0 || !P.work1 || !P.work2, PMK_ERR_ARG);
+  int rc = strided_copy(w, m, 0, out, (int64_t)nu * m, 0, m, nT + 1, live, s);
+  if (rc || nu == 1 || nT == 0) return rc;
+  const bool fft = P.fft_x != nullptr && (ny == 1 || P.fft_y != nullptr);
+  // forward transform of w[0..n_T) -> work1 (modes, y-mode slow)
+  if (fft) {
+    if (ny == 1) {
+      rc = launch_dst_rows(w, P.work1, nx, nT, P.fft_x, live, s);
+    } else {
+      rc = launch_dst_rows(w, P.work0, nx, (int64_t)nT * ny, P.fft_x, live, s);
+      if (!rc) rc = launch_dst_cols(P.work0, P.work1, nx, ny, nT, P.fft_y, live, s);
+    }
+  } else {
+    PMK_RETURN_IF(!P.sx || (ny > 1 && !P.sy), PMK_ERR_ARG);
+    if (ny == 1) {
+      rc = gemm(nT, nx, nx, w, nx, 0, P.sx, nx, 0, P.work1, nx, 0, 1, live, s);
+    } else {
+      rc = gemm(nT * ny, nx, nx, w, nx, 0, P.sx, nx, 0, P.work0, nx, 0, 1, live, s);
+      if (!rc) rc = gemm(ny, nx, ny, P.sy, ny, 0, P.work0, nx, m, P.work1, nx, m, nT, live, s);
+    }
+  }
+  if (rc) return rc;
+  const double scale = fft ? P.fft_scale : 1.0;
+  for (int j = 1; j < nu; ++j) {
+    {
+      prof::Scope sc(prof::kXfer, 16.0 * Nw, 0.0, s);
+      const int64_t g = (Nw + 255) / 256 < 16 * kSMs ? (Nw + 255) / 256 : 16 * kSMs;
+      mode_power_kernel<<<(int)g, 256, 0, s>>>(P.work1, P.work2, P.ratio, m, Nw, j, scale, live);
+    }
+    PMK_LAUNCH_CHECK();
+    double *dst = out + (int64_t)j * m;  // rows nu K + j, slice stride nu m
+    if (fft) {
+      if (ny == 1) {
+        rc = launch_dst_rows(P.work2, dst, nx, nT, P.fft_x, live, s, 1, (int64_t)nu * m);
+      } else {
+        rc = launch_dst_cols(P.work2, P.work0, nx, ny, nT, P.fft_y, live, s);
+        if (!rc)
+          rc = launch_dst_rows(P.work0, dst, nx, (int64_t)nT * ny, P.fft_x, live, s, ny,
+                               (int64_t)nu * m);
+      }
+    } else {
+      if (ny == 1) {
+        rc = gemm(1, nx, nx, P.work2, nx, m, P.sx, nx, 0, dst, nx, (int64_t)nu * m, nT, live, s);
+      } else {
+        rc = gemm(ny, nx, ny, P.sy, ny, 0, P.work2, nx, m, P.work0, nx, m, nT, live, s);
+        if (!rc)
+          rc = gemm(ny, nx, nx, P.work0, nx, m, P.sx, nx, 0, dst, nx, (int64_t)nu * m, nT, live,
+                    s);
+      }
+    }
+    if (rc) return rc;
+  }
+  return 0;
+}
 
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
                  cudaStream_t s) {

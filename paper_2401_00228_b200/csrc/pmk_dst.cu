@@ -167,7 +167,8 @@ __device__ __forceinline__ void load_tables(double2 *tw2, double2 *post, const d
 template <int LOGN>
 __global__ void __launch_bounds__(32 * kDstWarps)
     dst_rows_kernel(const double *__restrict__ in, double *__restrict__ out, int64_t rows,
-                    const double2 *gtw2, const double2 *gpost, const int *live) {
+                    int64_t rps, int64_t oss, const double2 *gtw2, const double2 *gpost,
+                    const int *live) {
   if (!is_live(live)) return;
   using P = Plan<LOGN>;
   constexpr int N = P::N, n = N - 1;
@@ -184,8 +185,10 @@ __global__ void __launch_bounds__(32 * kDstWarps)
        r0 += per_iter) {
     const int64_t r = r0 + h;
     const bool ok = r < rows;
-    const double *x = in + (ok ? r : 0) * n;
-    double *y = out + (ok ? r : 0) * n;
+    const int64_t rr = ok ? r : 0;
+    const double *x = in + rr * n;
+    // output row: slice rr / rps at stride oss (contiguous when oss = rps * n)
+    double *y = out + (rr / rps) * oss + (rr % rps) * n;
     dst_group<LOGN>([&](int j) { return ok ? __ldg(x + j) : 0.0; },
                     [&](int p, double v) {
                       if (ok) y[p - 1] = v;
@@ -260,7 +263,7 @@ int init_constants() {
 
 template <int LOGN, bool COLS>
 int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const double *tables,
-            const int *live, cudaStream_t s) {
+            const int *live, cudaStream_t s, int64_t rps = 0, int64_t oss = 0) {
   using P = Plan<LOGN>;
   constexpr int N = P::N;
   const int rc0 = init_constants();
@@ -269,8 +272,8 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
   if (COLS) smem += (size_t)(N - 1) * (kColTile + 1) * sizeof(double);
   void (*kern)(const double *, double *, int, int, const double2 *, const double2 *,
                const int *) = dst_cols_kernel<LOGN>;
-  void (*kern_r)(const double *, double *, int64_t, const double2 *, const double2 *,
-                 const int *) = dst_rows_kernel<LOGN>;
+  void (*kern_r)(const double *, double *, int64_t, int64_t, int64_t, const double2 *,
+                 const double2 *, const int *) = dst_rows_kernel<LOGN>;
   static int occ = -1;
   if (occ < 0) {
     int b = 0;
@@ -299,8 +302,14 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
   prof::Scope scope(prof::kGemm, 16.0 * elems, units * (5.0 * N * LOGN + 8.0 * N), s);
   if (COLS)
     kern<<<grid, 32 * kDstWarps, smem, s>>>(in, out, nx, (int)rows_or_slices, tw2, post, live);
-  else
-    kern_r<<<grid, 32 * kDstWarps, smem, s>>>(in, out, rows_or_slices, tw2, post, live);
+  else {
+    if (rps <= 0) {
+      rps = rows_or_slices;
+      oss = rows_or_slices * (N - 1);
+    }
+    kern_r<<<grid, 32 * kDstWarps, smem, s>>>(in, out, rows_or_slices, rps, oss, tw2, post,
+                                              live);
+  }
   PMK_LAUNCH_CHECK();
   return 0;
 }
@@ -317,17 +326,17 @@ int log2_exact(int n1) {
 // [N] w_N^{n2 k1} at [k1 * N2 + n2] (N2 = 2^floor(log2(N)/2)), then [N]
 // (cos, sin)(pi p / N), interleaved complex.
 int launch_dst_rows(const double *in, double *out, int n, int64_t rows, const double *tables,
-                    const int *live, cudaStream_t s) {
+                    const int *live, cudaStream_t s, int64_t rps, int64_t oss) {
   switch (log2_exact(n + 1)) {
-    case 2: return run_dst<2, false>(in, out, rows, 0, tables, live, s);
-    case 3: return run_dst<3, false>(in, out, rows, 0, tables, live, s);
-    case 4: return run_dst<4, false>(in, out, rows, 0, tables, live, s);
-    case 5: return run_dst<5, false>(in, out, rows, 0, tables, live, s);
-    case 6: return run_dst<6, false>(in, out, rows, 0, tables, live, s);
-    case 7: return run_dst<7, false>(in, out, rows, 0, tables, live, s);
-    case 8: return run_dst<8, false>(in, out, rows, 0, tables, live, s);
-    case 9: return run_dst<9, false>(in, out, rows, 0, tables, live, s);
-    case 10: return run_dst<10, false>(in, out, rows, 0, tables, live, s);
+    case 2: return run_dst<2, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 3: return run_dst<3, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 4: return run_dst<4, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 5: return run_dst<5, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 6: return run_dst<6, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 7: return run_dst<7, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 8: return run_dst<8, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 9: return run_dst<9, false>(in, out, rows, 0, tables, live, s, rps, oss);
+    case 10: return run_dst<10, false>(in, out, rows, 0, tables, live, s, rps, oss);
   }
   return PMK_ERR_UNSUPPORTED;
 }

@@ -151,6 +151,7 @@ struct MarchParams {
   // MVR
   double mu;
   int nu;
+  int inject;          // MVR: MGRIT injection (vh_K = s_{nu K}) instead of the time sum
   double *vh;          // (n_T+1, m) time-summed (fine spatial)
   double *v_norm_out;  // optional: the normalised input v = v_raw / scale
   // IMV
@@ -184,7 +185,13 @@ int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_s
 
 // ---------------------------------------------------------------- coarse
 int launch_dst_rows(const double *in, double *out, int n, int64_t rows, const double *tables,
-                    const int *live, cudaStream_t s);
+                    const int *live, cudaStream_t s, int64_t rows_per_slice = 0,
+                    int64_t out_slice_stride = 0);
+// MGRIT pair (pmk_coarse.cu): injection restriction / ideal interpolation
+int mgrit_restrict(const pmk_pair &P, const double *v, double *vh, const int *live,
+                   cudaStream_t s);
+int mgrit_interpolate(const pmk_pair &P, const double *w, double *out, const int *live,
+                      cudaStream_t s);
 int launch_dst_cols(const double *in, double *out, int nx, int ny, int slices,
                     const double *tables, const int *live, cudaStream_t s);
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,

@@ -174,7 +174,9 @@ __global__ void __launch_bounds__(256)
           } else if (MODE == kModeMVR) {
             if (p.v_norm_out) p.v_norm_out[e] = c;  // basis vector b/beta, w/h (solver.py:395,420)
             const double sv = __dsub_rn(o, __dmul_rn(p.mu, c));  // s -= mu * v
-            if (k == 0) {
+            if (p.inject) {
+              if (k % p.nu == 0) p.vh[(int64_t)(k / p.nu) * p.m + i] = sv;
+            } else if (k == 0) {
               p.vh[i] = sv;
             } else {
               const int pos = (k - 1) % p.nu;

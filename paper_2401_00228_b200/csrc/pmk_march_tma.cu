@@ -302,8 +302,12 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else if (MODE == kModeMVR) {
               if (p.v_norm_out) p.v_norm_out[kofs + gi] = cur;
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
-              acc[r] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[r], sval);
-              if (pos == nu - 1) p.vh[(int64_t)K * m + gi] = acc[r];
+              if (p.inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
+                if (k % nu == 0) p.vh[(int64_t)(k / nu) * m + gi] = sval;
+              } else {
+                acc[r] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[r], sval);
+                if (pos == nu - 1) p.vh[(int64_t)K * m + gi] = acc[r];
+              }
             } else {
               if (p.x_out) p.x_out[kofs + gi] = cur;
               if (p.out) p.out[kofs + gi] = o;

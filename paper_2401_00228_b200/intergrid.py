@@ -1,11 +1,11 @@
 """Intergrid pairs and coarse systems on the GPU.
 
-Mirror of reference ``pintmk/intergrid.py`` for the families on the MLK hot
-path: pure time coarsening (TimePair, Y = Z = nu-fold identity stacks) and
-simultaneous time-space coarsening by agglomeration (TimeSpacePair, Z
-piecewise-constant injection, Y agglomerate averaging), plus the perturbed
-decoupling of the coarsest level.  The MGRIT reduction pair is not on this
-path (SURVEY.md section 8(f) lists it as the next row).
+Mirror of reference ``pintmk/intergrid.py``: pure time coarsening (TimePair,
+Y = Z = nu-fold identity stacks), simultaneous time-space coarsening by
+agglomeration (TimeSpacePair, Z piecewise-constant injection, Y agglomerate
+averaging), the MGRIT reduction pair (MgritPair: injection and ideal
+interpolation) with its rediscretized coarse system, and the perturbed
+decoupling of the coarsest level.
 """
 
 from __future__ import annotations
@@ -159,6 +159,93 @@ class TimeSpacePair(_PairBase):
     def materialize(self):
         ys, zs = zip(*(self.block_matrices(k) for k in range(self.n_T + 1)))
         return sp.block_diag(ys, format="csr"), sp.block_diag(zs, format="csr")
+
+
+class MgritPair(_PairBase):
+    """Coarse-point injection with ideal interpolation (reference
+    intergrid.py:134-187): restrict keeps rows 0, nu, 2 nu, ...; interpolate
+    fills each slab by propagating its left coarse row through nu - 1 fine
+    steps, (psi^{-1} phi)^j, which the device applies in the sine basis of
+    the fine grid (diagonal there: ratio beta/delta per mode)."""
+
+    kind = "MGRIT"
+    partition = None
+
+    def __init__(self, ops: StepOperators, nu: int, n_T: int):
+        self.ops = ops
+        self.n = ops.n
+        self.m = ops.n
+        self.nu = nu
+        self.n_T = n_T
+        self.fine_rows = nu * n_T + 1
+        self._desc = None
+        self._keep = []
+
+    def _pair_desc(self) -> _lib.PairDesc:
+        if self._desc is None:
+            torch = _lib.require_cuda()
+            from .spatial import dst_eigenvalues_1d, dst_matrix, fft_dst_tables
+
+            sp_op, cfg = self.ops.spatial, self.ops.config
+            nx, ny = sp_op.n_x, (sp_op.n_y if sp_op.dim == 2 else 1)
+            ex = dst_eigenvalues_1d(nx)
+            lam = ex[None, :] if ny == 1 else (dst_eigenvalues_1d(ny)[:, None] + ex[None, :])
+            lam = (sp_op.tau / sp_op.delta_x**2) * lam.ravel()
+            delta = 1.0 - cfg.theta * cfg.delta_t * lam
+            beta = 1.0 + (1.0 - cfg.theta) * cfg.delta_t * lam
+            d = _lib.PairDesc()
+            d.nu, d.n_T, d.m_fine, d.m_coarse = self.nu, self.n_T, self.n, self.n
+            d.mgrit, d.dim, d.nx, d.ny = 1, sp_op.dim, nx, ny
+            keep = [torch.from_numpy(beta / delta).cuda()]
+            d.ratio = keep[0].data_ptr()
+            tabx = fft_dst_tables(nx)
+            taby = fft_dst_tables(ny) if ny > 1 else None
+            if tabx is not None and nx + 1 <= 1024 and (ny == 1 or (taby is not None
+                                                                     and ny + 1 <= 512)):
+                keep.append(torch.from_numpy(tabx).cuda())
+                d.fft_x = keep[-1].data_ptr()
+                d.fft_scale = 2.0 / (nx + 1)
+                if ny > 1:
+                    keep.append(torch.from_numpy(taby).cuda())
+                    d.fft_y = keep[-1].data_ptr()
+                    d.fft_scale *= 2.0 / (ny + 1)
+            else:
+                keep.append(torch.from_numpy(dst_matrix(nx)).cuda())
+                d.sx = keep[-1].data_ptr()
+                if ny > 1:
+                    keep.append(torch.from_numpy(dst_matrix(ny)).cuda())
+                    d.sy = keep[-1].data_ptr()
+                d.fft_scale = 1.0
+            nw = max(self.n_T, 1) * self.n
+            for name in ("work0", "work1", "work2"):
+                keep.append(torch.empty(nw, dtype=torch.float64, device="cuda"))
+                setattr(d, name, keep[-1].data_ptr())
+            keep.append(torch.empty((self.n_T + 1) * self.n, dtype=torch.float64, device="cuda"))
+            d.coarse_out = keep[-1].data_ptr()
+            self._keep = keep
+            self._desc = d
+        return self._desc
+
+
+def build_mgrit_pair(part) -> MgritPair:
+    return MgritPair(ops=part.fine.ops, nu=part.nu, n_T=part.n_T)
+
+
+def rediscretized_coarse(ops: StepOperators, nu: int, n_T: int) -> CoarseSystem:
+    """theta-scheme with step nu dt (reference intergrid.py:270-280): the
+    parareal coarse propagator, used with the reduction pair."""
+    from ._device import SpectralInfo
+
+    cfg = ops.config
+    big_dt = nu * cfg.delta_t
+    eye = sp.identity(ops.n, format="csr")
+    diag = (eye - cfg.theta * big_dt * ops.spatial.matrix).tocsr()
+    sub = (eye + (1 - cfg.theta) * big_dt * ops.spatial.matrix).tocsr()
+    sp_op = ops.spatial
+    return CoarseSystem(diag=diag, sub=sub, n_steps=n_T, provenance="rediscretized",
+                        grid=sp_op.grid, dim=sp_op.dim,
+                        spectral=SpectralInfo(sp_op.tau / sp_op.delta_x**2, cfg.theta * big_dt,
+                                              (1 - cfg.theta) * big_dt))
 
 
 def build_t_pair(n: int, nu: int, n_T: int) -> TimePair:

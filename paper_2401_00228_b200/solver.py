@@ -32,8 +32,8 @@ import scipy.sparse as sp
 
 from . import _lib
 from ._device import SpectralInfo
-from .intergrid import (CoarseSystem, TimePair, TimeSpacePair, agglomerate_partition,
-                        perturb_decouple)
+from .intergrid import (CoarseSystem, MgritPair, TimePair, TimeSpacePair,
+                        agglomerate_partition, perturb_decouple, rediscretized_coarse)
 from .spatial import gershgorin_bound
 from .stepper import BlockBidiagonalSystem, FineSystem, _to_device
 
@@ -273,8 +273,8 @@ def build_hierarchy(fine: FineSystem, n_levels: int, schedule: str | list[str] =
 
 def build_two_level(fine: FineSystem, family: str, nu: int,
                     cfg: SolverConfig | None = None) -> LevelHierarchy:
-    """Two-level hierarchy for the T or TS family (reference solver.py:238-265).
-    The MGRIT family is not on this path yet."""
+    """Two-level hierarchy for the T, TS or MGRIT family (reference
+    solver.py:238-265)."""
     cfg = cfg or SolverConfig()
     top = _fine_level(fine)
     if family == "T":
@@ -282,7 +282,14 @@ def build_two_level(fine: FineSystem, family: str, nu: int,
     elif family == "TS":
         coarse = _space_move(top, time_nu=nu)
     elif family == "MGRIT":
-        raise NotImplementedError("MGRIT intergrid family is not implemented on the GPU path")
+        if fine.n_t % nu != 0:
+            raise ValueError("nu must divide n_t")
+        n_T = fine.n_t // nu
+        top.pair = MgritPair(fine.ops, nu, n_T)
+        coarse = Level(system=rediscretized_coarse(fine.ops, nu, n_T),
+                       spatial_matrix=fine.ops.spatial.matrix, dt=nu * fine.ops.config.delta_t,
+                       implicit_weight=fine.ops.config.theta, n_steps=n_T, grid=top.grid,
+                       dim=top.dim, kind="mgrit", laplace_factor=top.laplace_factor)
     else:
         raise ValueError(f"unknown family {family!r}")
     if cfg.coarsest_n_cgs >= 1:
@@ -291,6 +298,12 @@ def build_two_level(fine: FineSystem, family: str, nu: int,
     hier.moves = [family]
     _setup_native(hier)
     return hier
+
+
+def _child_size(lvl: Level, nxt: Level) -> int:
+    """Per-iteration child buffer: the coarse solution, or for MGRIT pairs its
+    interpolation to the fine level (ideal interpolation is not a repeat)."""
+    return lvl.total_dim if isinstance(lvl.pair, MgritPair) else nxt.total_dim
 
 
 def _empty(n):
@@ -330,7 +343,7 @@ def _setup_native(hier: LevelHierarchy) -> None:
         else:
             rhs = _empty(lvl.total_dim)
             vs = [_empty(lvl.total_dim) for _ in range(lvl.budget)]
-            cos = [_empty(nxt.total_dim) for _ in range(lvl.budget)]
+            cos = [_empty(_child_size(lvl, nxt)) for _ in range(lvl.budget)]
             wb = _empty(lvl.total_dim)
         keep += [rhs, vs, cos, wb, ts]
         n = len(vs)
@@ -355,7 +368,7 @@ def apply_preconditioner(hier: LevelHierarchy, level_idx: int, v, ledger=None, m
     if dv.numel() != lvl.total_dim:
         raise ValueError("vector size does not match the level")
     out = _empty(lvl.total_dim)
-    child = _empty(nxt.total_dim)
+    child = _empty(_child_size(lvl, nxt))
     lib = _lib.load()
     _lib.check(lib.pmk_apply_preconditioner(hier._native, level_idx, _lib.ptr(dv),
                                             _lib.ptr(child), _lib.ptr(out), _lib.stream_ptr()),
@@ -427,14 +440,15 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
     if st["beta"] == 0.0:
         return torch.zeros_like(b), report
     vs, cos = [], []
-    per_iter = 8 * (lvl.total_dim + nxt.total_dim)
+    csize = _child_size(lvl, nxt)
+    per_iter = 8 * (lvl.total_dim + csize)
     budget = _MemoryBudget()
     budget.take(8 * lvl.total_dim)
     w = _empty(lvl.total_dim)  # unnormalised new vector, reused every iteration
     for j in range(max_iter):
         budget.take(per_iter)
         v = _empty(lvl.total_dim)
-        co = _empty(nxt.total_dim)
+        co = _empty(csize)
         vs.append(v)
         cos.append(co)
         _lib.check(lib.pmk_fgmres_step(H, level_idx, j, _lib.ptr(v), _lib.ptr(w), _lib.ptr(co),
@@ -455,7 +469,9 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
         basis = [vs[l].cpu().numpy() for l in range(n_iter)]
         if not st["breakdown"]:
             basis.append(w.cpu().numpy() / st["hraw"][n_iter, n_iter - 1])  # IEEE division
-        pre = [(vs[l] - lvl.pair.interpolate(cos[l])).cpu().numpy() for l in range(n_iter)]
+        mg = isinstance(lvl.pair, MgritPair)  # cos already hold the interpolated vectors
+        pre = [(vs[l] - (cos[l] if mg else lvl.pair.interpolate(cos[l]))).cpu().numpy()
+               for l in range(n_iter)]
         report.metadata["basis"] = basis
         report.metadata["preconditioned"] = pre
         report.metadata["hessenberg"] = st["hraw"][:n_iter + 1, :n_iter].copy()

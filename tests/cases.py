@@ -118,6 +118,13 @@ SMALL = {
     # 2-level TS family (build_two_level)
     "ts2_small": Case("ts2_small", 1, 31, 32, 0.5, 2, ("TS",), courant=0.64,
                       two_level_family="TS", max_outer=40),
+    # 2-level MGRIT family (build_two_level; injection + ideal interpolation)
+    "mgrit1_small": Case("mgrit1_small", 1, 31, 32, 0.5, 2, ("MGRIT",), nu=4, courant=0.64,
+                         two_level_family="MGRIT", max_outer=40),
+    "mgrit2_small": Case("mgrit2_small", 2, 15, 32, 0.5, 2, ("MGRIT",), nu=2, courant=0.16,
+                         two_level_family="MGRIT", max_outer=40),
+    "mgrit2_dec_small": Case("mgrit2_dec_small", 2, 15, 48, 1.0, 2, ("MGRIT",), nu=3,
+                             courant=0.16, two_level_family="MGRIT", n_cgs=4, max_outer=40),
 }
 
 # BASELINE.json configs (literal) and their regime-adjusted companions.
@@ -150,6 +157,9 @@ def oracle_hierarchy(case: Case):
     cfg = O.Config(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
                    inner_iters=case.inner_iters, coarsest_n_cgs=case.n_cgs,
                    restart=case.restart)
+    if case.two_level_family == "MGRIT":
+        return O.build_mgrit(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
+                             case.u0_vector(), cfg, nu=case.nu)
     if case.two_level_family is not None:
         fam = {"T": ["time"], "TS": ["time_space"]}[case.two_level_family]
         return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,

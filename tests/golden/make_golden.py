@@ -118,8 +118,10 @@ def record(case) -> dict:
     return out
 
 
-def main():
+def main(names=None):
     for name, case in SMALL.items():
+        if names and name not in names:
+            continue
         data = record(case)
         path = os.path.join(HERE, f"{name}.npz")
         np.savez_compressed(path, **data)
@@ -128,4 +130,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

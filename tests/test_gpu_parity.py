@@ -50,11 +50,20 @@ def test_matvec_bitwise(name):
 
 @pytest.mark.parametrize("name", sorted(SMALL))
 def test_transfers_bitwise(name):
+    """Restrictions are bitwise; interpolations are bitwise except the MGRIT
+    family's ideal interpolation, whose (psi^{-1} phi)^j propagation runs in
+    the sine basis (reference: per-step LU/Thomas solves): <= 1e-13."""
+    from paper_2401_00228_b200.intergrid import MgritPair
+
     g = golden(name)
     h = gpu_hierarchy(SMALL[name])
     for i, lv in enumerate(h.levels[:-1]):
         np.testing.assert_array_equal(lv.pair.restrict(g[f"r{i}_in"]), g[f"r{i}_out"])
-        np.testing.assert_array_equal(lv.pair.interpolate(g[f"i{i}_in"]), g[f"i{i}_out"])
+        out = lv.pair.interpolate(g[f"i{i}_in"])
+        if isinstance(lv.pair, MgritPair):
+            assert rel(out, g[f"i{i}_out"]) <= 1e-13, rel(out, g[f"i{i}_out"])
+        else:
+            np.testing.assert_array_equal(out, g[f"i{i}_out"])
 
 
 @pytest.mark.parametrize("name", sorted(SMALL))
