@@ -22,9 +22,12 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
+#include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "pmk_internal.cuh"
@@ -99,6 +102,10 @@ struct LevelRT {
   int cap = 0;
   double *partA = nullptr, *partB = nullptr;
   double tol = 0.0;
+  // CUDA graphs of this level's inner solve, keyed by its output buffer
+  std::unordered_set<const double *> seen;
+  std::unordered_map<const double *, std::pair<cudaGraphExec_t, int64_t>> graphs;
+  bool graph_failed = false;
   // current invocation
   const double *rhs_cur = nullptr;   // rhs of this invocation (raw basis vector 0)
   const double *pending = nullptr;   // unnormalised basis vector j (w of iteration j-1)
@@ -277,6 +284,61 @@ int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double t
 
 int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s);
 
+bool graphs_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("PMK_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return on && !g_prof_on;
+}
+
+// The inner FGMRES recursion below a level (solver.py:347-348) touches only
+// registered buffers plus its output, and never synchronises with the host,
+// so it is captured once per output buffer into a CUDA graph and replayed
+// (the first call runs eagerly so that lazy one-time initialisation -- kernel
+// attributes, constant tables -- never happens inside a capture).
+int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cudaStream_t s) {
+  LevelRT &R = H->lv[child];
+  if (!graphs_enabled() || R.graph_failed || s == nullptr || s == cudaStreamLegacy ||
+      s == cudaStreamPerThread)
+    return fgmres_fixed(H, child, out, live, s);
+  auto it = R.graphs.find(out);
+  if (it != R.graphs.end()) {
+    g_launches.fetch_add(it->second.second);  // the graph's kernel nodes
+    PMK_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
+    return 0;
+  }
+  if (!R.seen.count(out)) {
+    R.seen.insert(out);
+    return fgmres_fixed(H, child, out, live, s);
+  }
+  const int64_t before = g_launches.load();
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    R.graph_failed = true;
+    return fgmres_fixed(H, child, out, live, s);
+  }
+  int rc = fgmres_fixed(H, child, out, live, s);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &g);
+  const int64_t nodes = g_launches.load() - before;
+  g_launches.store(before);  // captured launches are counted when replayed
+  cudaGraphExec_t exec = nullptr;
+  if (rc == 0 && e == cudaSuccess && g &&
+      cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
+    cudaGraphDestroy(g);
+    R.graphs[out] = {exec, nodes};
+    g_launches.fetch_add(nodes);
+    PMK_CUDA_TRY(cudaGraphLaunch(exec, s));
+    return 0;
+  }
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  R.graph_failed = true;
+  if (rc) return rc;
+  return fgmres_fixed(H, child, out, live, s);
+}
+
 // Child solve of level idx: vt = A_{idx+1}^{-1} vh (approximately).
 int child_solve(pmk_hier *H, int idx, double *out, const int *live, cudaStream_t s) {
   const int child = idx + 1;
@@ -284,6 +346,7 @@ int child_solve(pmk_hier *H, int idx, double *out, const int *live, cudaStream_t
     PMK_RETURN_IF(!H->has_coarse || !H->coarse_rhs, PMK_ERR_STATE);
     return coarse_solve(H->coarse, H->coarse_rhs, out, live, s);
   }
+  if (idx == 0) return fgmres_fixed_graph(H, child, out, live, s);
   return fgmres_fixed(H, child, out, live, s);
 }
 
@@ -550,8 +613,10 @@ pmk_hier *pmk_hier_create(int32_t n_levels, double mu) {
 
 void pmk_hier_destroy(pmk_hier *H) {
   if (!H) return;
-  for (auto &R : H->lv)
+  for (auto &R : H->lv) {
+    for (auto &kv : R.graphs) cudaGraphExecDestroy(kv.second.first);
     if (R.d_block) cudaFree(R.d_block);
+  }
   delete H;
 }
 

@@ -22,8 +22,8 @@ real time.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
-import math
 import time
 from dataclasses import dataclass, field
 
@@ -117,6 +117,25 @@ class LevelHierarchy:
         self.moves: list[str] = []
         self._native = None
         self._buffers: list = []
+        self._stream = None
+
+    @contextlib.contextmanager
+    def on_stream(self):
+        """Run on the hierarchy's own CUDA stream (the inner recursion is
+        replayed as CUDA graphs, which cannot be captured on the legacy
+        default stream); ordered after / before the caller's stream."""
+        import torch
+
+        if self._stream is None:
+            self._stream = torch.cuda.Stream()
+        caller = torch.cuda.current_stream()
+        if caller == self._stream:
+            yield
+            return
+        self._stream.wait_stream(caller)
+        with torch.cuda.stream(self._stream):
+            yield
+        caller.wait_stream(self._stream)
 
     @property
     def n_levels(self) -> int:
@@ -360,6 +379,11 @@ def _setup_native(hier: LevelHierarchy) -> None:
 # --------------------------------------------------------------------- solve
 def apply_preconditioner(hier: LevelHierarchy, level_idx: int, v, ledger=None, model=None):
     """v - Z A_H^{-1} Y^T (A v - mu v) at one level (reference solver.py:323-359)."""
+    with hier.on_stream():
+        return _apply_preconditioner(hier, level_idx, v)
+
+
+def _apply_preconditioner(hier: LevelHierarchy, level_idx: int, v):
     if not 0 <= level_idx < hier.n_levels - 1:
         raise ValueError("level_idx must index a non-coarsest level")
     shape = tuple(v.shape) if hasattr(v, "shape") else np.shape(v)
@@ -420,6 +444,12 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
     """Right-preconditioned FGMRES, MGS + Givens, zero initial guess, no
     restarts (reference solver.py:362-456).  tol=None runs exactly max_iter
     iterations (inner solves) unless the basis breaks down."""
+    with hier.on_stream():
+        return _fgmres(hier, level_idx, rhs, tol, max_iter, keep_basis)
+
+
+def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_iter: int,
+            keep_basis: bool = False):
     import torch
 
     if not 0 <= level_idx < hier.n_levels - 1:
@@ -499,7 +529,7 @@ def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart:
             converged = True
             break
         m = min(restart, max_outer - total)
-        dx, rep = fgmres(hier, 0, r, tol=tol * beta0 / rn, max_iter=m)
+        dx, rep = _fgmres(hier, 0, r, tol=tol * beta0 / rn, max_iter=m)
         x = x + dx
         total += rep.outer_iterations
         cycles += 1
@@ -537,10 +567,11 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     rhs = hier.fine.rhs.reshape(-1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    if cfg.restart is None:
-        x, report = fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer)
-    else:
-        x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart)
+    with hier.on_stream():
+        if cfg.restart is None:
+            x, report = _fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer)
+        else:
+            x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart)
     torch.cuda.synchronize()
     report.method = method_name
     report.wall_time = time.perf_counter() - t0
