@@ -14,7 +14,8 @@ import subprocess
 from ctypes import POINTER, c_double, c_int32, c_int64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpmk_b200.so")
+# PMK_LIB overrides the library path (tuning builds, e.g. libpmk_b200_<variant>.so)
+LIB_PATH = os.environ.get("PMK_LIB") or os.path.join(_HERE, "libpmk_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 PMK_ERR_ARG = 1001

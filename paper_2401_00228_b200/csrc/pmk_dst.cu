@@ -23,8 +23,8 @@
 //   shared-memory FFT moves ~5 N log2 N); 32 / N2 transforms run per warp,
 //   synchronised with __syncwarp only.
 // x-direction: rows contiguous, groups of N2 lanes per row.
-// y-direction: a CTA stages a (ny x 32) column tile of one slice (coalesced
-// 256-byte row segments) and transforms its 32 columns from shared memory.
+// y-direction: a CTA stages a (ny x 16) column tile of one slice (coalesced
+// 128-byte row segments) and transforms its 16 columns from shared memory.
 // Unnormalised: applying it twice gives (N/2) x; the solver folds the
 // orthonormal factors into the recurrence.
 #include <cmath>
@@ -35,8 +35,14 @@
 namespace pmk {
 namespace {
 
-constexpr int kDstWarps = 4;
-constexpr int kColTile = 32;
+#ifndef PMK_DST_WARPS
+#define PMK_DST_WARPS 8
+#endif
+#ifndef PMK_DST_COLTILE
+#define PMK_DST_COLTILE 16
+#endif
+constexpr int kDstWarps = PMK_DST_WARPS;
+constexpr int kColTile = PMK_DST_COLTILE;
 
 // e^{-2 pi i j / 32}, j < 32: radix-2 twiddles of every in-register FFT
 // (length L <= 32 uses entries j * 32 / L).
