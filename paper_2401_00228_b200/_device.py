@@ -167,8 +167,8 @@ class CoarseSolver:
             d.beta = tabs[2].data_ptr()
             self._keep += tabs
             self.work0 = torch.empty(self.N, dtype=torch.float64, device="cuda")
-            self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda") \
-                if self.ny > 1 else None
+            # 2-D: second transform buffer; 1-D: chunked-recurrence scratch
+            self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
             self.kind = "dst"
         else:
             if self.m > DENSE_MAX_M:

@@ -101,6 +101,7 @@ struct LevelRT {
   void *d_block = nullptr;
   int cap = 0;
   double *partA = nullptr, *partB = nullptr;
+  double *partM = nullptr;  // ICWY dot partials
   double tol = 0.0;
   // CUDA graphs of this level's inner solve, keyed by its output buffer
   std::unordered_set<const double *> seen;
@@ -226,7 +227,10 @@ int alloc_state(LevelRT &R, int cap) {
     R.d_block = nullptr;
   }
   const size_t nh = (size_t)(cap + 1) * cap;
-  const size_t n_doubles = 2 * nh + 7 * (size_t)(cap + 1) + 2 * kMaxPartials;
+  const size_t n_groups = (size_t)(cap + kDotGroup - 1) / kDotGroup;
+  const size_t n_dotp = n_groups * (2 * kDotGroup + 1) * kMaxPartials;
+  const size_t n_doubles =
+      2 * nh + (size_t)cap * cap + 7 * (size_t)(cap + 1) + 2 * kMaxPartials + n_dotp;
   const size_t bytes = sizeof(KState) + 64 + n_doubles * sizeof(double);
   PMK_CUDA_TRY(cudaMalloc(&R.d_block, bytes));
   PMK_CUDA_TRY(cudaMemset(R.d_block, 0, bytes));
@@ -254,6 +258,10 @@ int alloc_state(LevelRT &R, int cap) {
   R.partA = d;
   d += kMaxPartials;
   R.partB = d;
+  d += kMaxPartials;
+  h.gram = d;
+  d += (size_t)cap * cap;
+  R.partM = d;
   R.h_state = h;
   R.cap = cap;
   PMK_CUDA_TRY(cudaMemcpy(R.d_state, &h, sizeof(KState), cudaMemcpyHostToDevice));
@@ -356,6 +364,15 @@ double *child_rhs(pmk_hier *H, int idx) {
   return H->lv[child].rhs;
 }
 
+// PMK_MGS=classic: sequential MGS passes (bitwise the reference's Hessenberg)
+bool classic_mgs() {
+  static const bool on = [] {
+    const char *e = getenv("PMK_MGS");
+    return e && std::strcmp(e, "classic") == 0;
+  }();
+  return on;
+}
+
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
                 cudaStream_t s) {
   LevelRT &R = H->lv[idx];
@@ -387,7 +404,19 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   rc = do_imv(R.L, R.P, v_out, nullptr, child_out, nullptr, w_next, R.v[0], nullptr, R.partA,
               &np, live, s);
   if (rc) return rc;
-  // MGS (solver.py:405-408), then ||w|| on the last pass (solver.py:412)
+  if (!classic_mgs()) {
+    // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412)
+    int n_norm = 0;
+    rc = launch_icwy_mgs(R.d_state, R.cap, j, w_next, R.v.data(), R.N, R.partA, np, R.partM,
+                         R.partB, &n_norm, s);
+    if (rc) return rc;
+    rc = launch_finish_col(R.d_state, R.cap, j, R.partB, n_norm, R.tol, s);
+    if (rc) return rc;
+    R.pending = w_next;
+    R.vt.push_back(child_out);
+    return 0;
+  }
+  // MGS one basis vector per pass, exactly the reference's operation order
   double *prev = R.partA, *cur = R.partB;
   int n_prev = np;
   for (int l = 0; l <= j; ++l) {

@@ -149,6 +149,83 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Chunked form of the same recurrence for few modes (1-D coarsest levels):
+// u_k = a_k u_{k-1} + b_k with a_k = beta/delta (0 at dropped rows) and
+// b_k = scale r^_k / delta.  Pass 1: every (mode, chunk) runs the chunk from a
+// zero state and stores its end value and the chunk's product of a_k.  Pass
+// 2: every (mode, chunk) combines the carries of the preceding chunks (at
+// most n_chunks steps), then re-runs its chunk from the carried state.
+__global__ void rec_chunk_pass1(const double *X, const double *delta, const double *beta,
+                                const uint8_t *dropped, int n_steps, int m, double scale,
+                                int clen, int nch, double *carryB, double *carryA,
+                                const int *live) {
+  if (!is_live(live)) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * nch) return;
+  const int i = (int)(t % m), c = (int)(t / m);
+  const double d = 1.0 / delta[i], a = beta[i] * d;
+  const int k0 = 1 + c * clen, k1 = min(n_steps + 1, k0 + clen);
+  double u = 0.0, P = 1.0;
+  for (int k = k0; k < k1; ++k) {
+    const bool cut = dropped && dropped[k];
+    const double bk = X[(int64_t)k * m + i] * scale * d;
+    u = cut ? bk : fma(a, u, bk);
+    P = cut ? 0.0 : P * a;
+  }
+  carryB[t] = u;
+  carryA[t] = P;
+}
+
+__global__ void rec_chunk_pass2(double *X, const double *delta, const double *beta,
+                                const uint8_t *dropped, int n_steps, int m, double scale,
+                                int clen, int nch, const double *carryB, const double *carryA,
+                                const int *live) {
+  if (!is_live(live)) return;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * nch) return;
+  const int i = (int)(t % m), c = (int)(t / m);
+  const double d = 1.0 / delta[i], a = beta[i] * d;
+  double u = X[i] * scale;  // slice 0 (transformed rhs_0)
+  for (int q = 0; q < c; ++q) u = fma(carryA[(int64_t)q * m + i], u, carryB[(int64_t)q * m + i]);
+  const int k0 = 1 + c * clen, k1 = min(n_steps + 1, k0 + clen);
+  for (int k = k0; k < k1; ++k) {
+    const bool cut = dropped && dropped[k];
+    const double bk = X[(int64_t)k * m + i] * scale * d;
+    u = cut ? bk : fma(a, u, bk);
+    X[(int64_t)k * m + i] = u;
+  }
+  if (c == 0) X[i] = X[i] * scale;
+}
+
+// Recurrence launcher: per-mode sequential scan when there are enough modes
+// to fill the GPU, chunked two-pass scan otherwise.
+int run_recurrence(const pmk_coarse &C, double *X, int m, double scale, double *scratch,
+                   const int *live, cudaStream_t s) {
+  const int64_t N = (int64_t)(C.n_steps + 1) * m;
+  prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
+  if (m >= 16 * 1024 || !scratch || C.n_steps < 64) {
+    dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(X, C.delta, C.beta, C.dropped,
+                                                         C.n_steps, m, scale, live);
+    PMK_LAUNCH_CHECK();
+    return 0;
+  }
+  int nch = (int)((64LL * 1024 + m - 1) / m);  // ~64 K threads
+  if (nch > C.n_steps / 8) nch = C.n_steps / 8;
+  const int clen = (C.n_steps + nch - 1) / nch;
+  nch = (C.n_steps + clen - 1) / clen;
+  double *cB = scratch, *cA = scratch + (int64_t)m * nch;
+  const int64_t th = (int64_t)m * nch;
+  rec_chunk_pass1<<<(int)((th + 255) / 256), 256, 0, s>>>(X, C.delta, C.beta, C.dropped,
+                                                          C.n_steps, m, scale, clen, nch, cB, cA,
+                                                          live);
+  PMK_LAUNCH_CHECK();
+  rec_chunk_pass2<<<(int)((th + 255) / 256), 256, 0, s>>>(X, C.delta, C.beta, C.dropped,
+                                                          C.n_steps, m, scale, clen, nch, cB, cA,
+                                                          live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
 __global__ void copy_row_kernel(const double *src, double *dst, int m, const int *live) {
   if (!is_live(live)) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
@@ -325,13 +402,8 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     if (ny == 1) {
       rc = launch_dst_rows(rhs, C.work0, nx, rows, C.fft_x, live, s);
       if (rc) return rc;
-      {
-        prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
-        dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta,
-                                                             C.dropped, C.n_steps, m,
-                                                             C.fft_scale, live);
-      }
-      PMK_LAUNCH_CHECK();
+      rc = run_recurrence(C, C.work0, m, C.fft_scale, C.work1, live, s);
+      if (rc) return rc;
       rc = launch_dst_rows(C.work0, out, nx, rows, C.fft_x, live, s);
       if (rc) return rc;
     } else {

@@ -208,6 +208,292 @@ __global__ void __launch_bounds__(kRedThreads)
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// ------------------------------------------------- one-reduce MGS (ICWY)
+// The reference orthogonalises w against v_0..v_j one vector at a time
+// (solver.py:405-408): h_i = <w^(i), v_i>, w^(i+1) = w^(i) - h_i v_i, which
+// streams ~4 vectors per basis vector.  In exact arithmetic
+//   h_i = <w, v_i> - sum_{l<i} h_l <v_l, v_i>,   i.e.  (I + L) h = V^T w
+// with L the strictly lower triangle of the basis Gram matrix, so h follows
+// from ONE pass of dot products (V^T w, plus the new Gram row <v_j, v_i>
+// while v_j streams by anyway) and w from ONE update pass applying the
+// subtractions in the reference's order with the reference's per-element
+// rounding.  This is the inverse-compact-WY form of MGS (Swirydowicz et al.,
+// "Low synchronization Gram-Schmidt and GMRES algorithms"), whose loss of
+// orthogonality is that of MGS; ~2 vectors per basis vector are streamed.
+// Update passes take up to kGroup basis vectors each, dot passes kDotGroup
+// (two accumulators per vector).
+
+// Deterministic block reduction of NV per-thread values; thread v < NV
+// writes value v's block sum to out[v * out_stride].
+template <int NV>
+__device__ __forceinline__ void block_sum_multi(double (&a)[NV], double *out, int out_stride) {
+  __shared__ double red[kRedThreads / 32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double x = a[v];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+    if (lane == 0) red[warp][v] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double x = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) x = __dadd_rn(x, red[w][threadIdx.x]);
+    out[(int64_t)threadIdx.x * out_stride] = x;
+  }
+}
+
+__device__ __forceinline__ double dot2(double acc, double2 a, double2 b) {
+  acc = __dadd_rn(acc, __dmul_rn(a.x, b.x));
+  return __dadd_rn(acc, __dmul_rn(a.y, b.y));
+}
+
+// Partials of <w, v_q> (slot q), <vj, v_q> (slot kDotGroup + q) for the
+// group, and <w, vj> (slot 2 kDotGroup); slot s at partials[s * gridDim.x].
+// Aligned operands: CNT vectors, U element steps per trip so that ~12
+// 16-byte loads are in flight per thread whatever the group size.
+template <int CNT>
+__global__ void __launch_bounds__(kRedThreads)
+    icwy_dots_vec_kernel(const KState *st, const double *__restrict__ w,
+                         const double *__restrict__ vj, MultiVec V, int64_t n,
+                         double *partials) {
+  if (!st->live) return;
+  constexpr int U = (12 / (CNT + 2)) > 1 ? 12 / (CNT + 2) : 1;
+  double aw[CNT], ag[CNT], awj[1] = {0.0};
+#pragma unroll
+  for (int q = 0; q < CNT; ++q) aw[q] = ag[q] = 0.0;
+  const double2 *w2 = reinterpret_cast<const double2 *>(w);
+  const double2 *j2 = reinterpret_cast<const double2 *>(vj);
+  const double2 *c2[CNT];
+#pragma unroll
+  for (int q = 0; q < CNT; ++q) c2[q] = reinterpret_cast<const double2 *>(V.v[q]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n2 = n >> 1;
+  int64_t i = t0;
+  for (; i + (U - 1) * stride < n2; i += U * stride) {
+    double2 a[U], b[U], c[U][CNT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = __ldg(w2 + i + u * stride);
+      b[u] = __ldg(j2 + i + u * stride);
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) c[u][q] = __ldg(c2[q] + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      awj[0] = dot2(awj[0], a[u], b[u]);
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) {
+        aw[q] = dot2(aw[q], a[u], c[u][q]);
+        ag[q] = dot2(ag[q], b[u], c[u][q]);
+      }
+    }
+  }
+  for (; i < n2; i += stride) {
+    const double2 a = __ldg(w2 + i), b = __ldg(j2 + i);
+    awj[0] = dot2(awj[0], a, b);
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) {
+      const double2 c = __ldg(c2[q] + i);
+      aw[q] = dot2(aw[q], a, c);
+      ag[q] = dot2(ag[q], b, c);
+    }
+  }
+  if ((n & 1) && t0 == stride - 1) {
+    const double a = w[n - 1], b = vj[n - 1];
+    awj[0] = __dadd_rn(awj[0], __dmul_rn(a, b));
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) {
+      const double c = V.v[q][n - 1];
+      aw[q] = __dadd_rn(aw[q], __dmul_rn(a, c));
+      ag[q] = __dadd_rn(ag[q], __dmul_rn(b, c));
+    }
+  }
+  double *out = partials + blockIdx.x;
+  block_sum_multi<CNT>(aw, out, gridDim.x);
+  __syncthreads();
+  block_sum_multi<CNT>(ag, out + (int64_t)kDotGroup * gridDim.x, gridDim.x);
+  __syncthreads();
+  block_sum_multi<1>(awj, out + (int64_t)2 * kDotGroup * gridDim.x, gridDim.x);
+}
+
+// Any alignment, runtime group size.
+__global__ void __launch_bounds__(kRedThreads)
+    icwy_dots_kernel(const KState *st, const double *__restrict__ w,
+                     const double *__restrict__ vj, MultiVec V, int count, int64_t n,
+                     double *partials) {
+  if (!st->live) return;
+  double aw[kDotGroup], ag[kDotGroup], awj[1] = {0.0};
+#pragma unroll
+  for (int q = 0; q < kDotGroup; ++q) aw[q] = ag[q] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double a = w[i], b = vj[i];
+    awj[0] = __dadd_rn(awj[0], __dmul_rn(a, b));
+#pragma unroll
+    for (int q = 0; q < kDotGroup; ++q)
+      if (q < count) {
+        const double c = V.v[q][i];
+        aw[q] = __dadd_rn(aw[q], __dmul_rn(a, c));
+        ag[q] = __dadd_rn(ag[q], __dmul_rn(b, c));
+      }
+  }
+  double *out = partials + blockIdx.x;
+  block_sum_multi<kDotGroup>(aw, out, gridDim.x);
+  __syncthreads();
+  block_sum_multi<kDotGroup>(ag, out + (int64_t)kDotGroup * gridDim.x, gridDim.x);
+  __syncthreads();
+  block_sum_multi<1>(awj, out + (int64_t)2 * kDotGroup * gridDim.x, gridDim.x);
+}
+
+// warp-level deterministic sum of n partials (fixed lane order + xor tree)
+__device__ __forceinline__ double warp_reduce_partials(const double *p, int n) {
+  const int lane = threadIdx.x & 31;
+  double x = 0.0;
+  for (int i = lane; i < n; i += 32) x = __dadd_rn(x, p[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// Reduce the dot partials, store Gram row j, solve (I + L) h = c and write
+// column j of H (rows 0..j).  One block.
+//   c_0 = <w, v_0>: K-IMV partials (c0p, n_c0); for j >= 1 the group passes
+//   wrote, per group g (basis 0..j-1 in groups of kGroup, slots as above),
+//   <w, v_i> for i >= 1, <v_j, v_i>, and <w, v_j> (taken from group 0).
+__global__ void __launch_bounds__(1024)
+    icwy_solve_kernel(KState *st, int ld, int j, const double *c0p, int n_c0,
+                      const double *gp, int n_gp) {
+  if (!st->live) return;
+  extern __shared__ double sh[];  // c[0..j], g[0..j-1]
+  double *c = sh, *g = sh + (j + 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gstride = (2 * kDotGroup + 1) * n_gp;  // doubles per group
+  for (int d = warp; d < 2 * j + 1; d += nw) {
+    double x;
+    if (d == 0) {
+      x = warp_reduce_partials(c0p, n_c0);
+    } else if (d < j) {  // <w, v_d>, 1 <= d < j
+      x = warp_reduce_partials(gp + (int64_t)(d / kDotGroup) * gstride + (d % kDotGroup) * n_gp, n_gp);
+    } else if (d == j) {  // <w, v_j>
+      x = warp_reduce_partials(gp + (int64_t)2 * kDotGroup * n_gp, n_gp);
+    } else {  // <v_j, v_i>, i = d - j - 1
+      const int i = d - j - 1;
+      x = warp_reduce_partials(
+          gp + (int64_t)(i / kDotGroup) * gstride + (kDotGroup + i % kDotGroup) * n_gp, n_gp);
+    }
+    if (lane == 0) {
+      if (d <= j)
+        c[d] = x;
+      else
+        g[d - j - 1] = x;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < j; i += blockDim.x) st->gram[(int64_t)j * ld + i] = g[i];
+  if (warp != 0) return;
+  // forward substitution, row i of L = Gram row i (stored at iteration i)
+  double *h = st->h;
+  for (int i = 0; i <= j; ++i) {
+    const double *Li = (i == j) ? g : st->gram + (int64_t)i * ld;
+    double x = 0.0;
+    for (int l = lane; l < i; l += 32) x = __dadd_rn(x, __dmul_rn(Li[l], c[l]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = __dadd_rn(x, __shfl_xor_sync(0xffffffffu, x, o));
+    // c[l] for l < i already holds h_l
+    const double hi = __dsub_rn(c[i], x);
+    __syncwarp();
+    if (lane == 0) {
+      c[i] = hi;
+      h[(int64_t)i * ld + j] = hi;
+    }
+    __syncwarp();
+  }
+}
+
+// w -= sum_q h[i0+q][j] v_q (ascending q, the reference's per-element
+// rounding); with `partials`, the partial sums of ||w||^2 of the result.
+template <int CNT>
+__global__ void __launch_bounds__(kRedThreads)
+    icwy_update_vec_kernel(const KState *st, int ld, int j, int i0, MultiVec V,
+                           double *__restrict__ w, int64_t n, double *partials) {
+  if (!st->live) return;
+  constexpr int U = (12 / (CNT + 1)) > 1 ? 12 / (CNT + 1) : 1;
+  double hq[CNT];
+  const double2 *c2[CNT];
+#pragma unroll
+  for (int q = 0; q < CNT; ++q) {
+    hq[q] = st->h[(int64_t)(i0 + q) * ld + j];
+    c2[q] = reinterpret_cast<const double2 *>(V.v[q]);
+  }
+  double acc[1] = {0.0};
+  double2 *w2 = reinterpret_cast<double2 *>(w);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n2 = n >> 1;
+  int64_t i = t0;
+  for (; i + (U - 1) * stride < n2; i += U * stride) {
+    double2 a[U], c[U][CNT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = w2[i + u * stride];
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) c[u][q] = __ldg(c2[q] + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) {
+        a[u].x = __dsub_rn(a[u].x, __dmul_rn(hq[q], c[u][q].x));
+        a[u].y = __dsub_rn(a[u].y, __dmul_rn(hq[q], c[u][q].y));
+      }
+      w2[i + u * stride] = a[u];
+      if (partials) acc[0] = dot2(acc[0], a[u], a[u]);
+    }
+  }
+  for (; i < n2; i += stride) {
+    double2 a = w2[i];
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) {
+      const double2 c = __ldg(c2[q] + i);
+      a.x = __dsub_rn(a.x, __dmul_rn(hq[q], c.x));
+      a.y = __dsub_rn(a.y, __dmul_rn(hq[q], c.y));
+    }
+    w2[i] = a;
+    if (partials) acc[0] = dot2(acc[0], a, a);
+  }
+  if ((n & 1) && t0 == stride - 1) {
+    double a = w[n - 1];
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) a = __dsub_rn(a, __dmul_rn(hq[q], V.v[q][n - 1]));
+    w[n - 1] = a;
+    if (partials) acc[0] = __dadd_rn(acc[0], __dmul_rn(a, a));
+  }
+  if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(kRedThreads)
+    icwy_update_kernel(const KState *st, int ld, int j, int i0, MultiVec V, int count,
+                       double *__restrict__ w, int64_t n, double *partials) {
+  if (!st->live) return;
+  double hq[kGroup];
+#pragma unroll
+  for (int q = 0; q < kGroup; ++q) hq[q] = (q < count) ? st->h[(int64_t)(i0 + q) * ld + j] : 0.0;
+  double acc[1] = {0.0};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double a = w[i];
+#pragma unroll
+    for (int q = 0; q < kGroup; ++q)
+      if (q < count) a = __dsub_rn(a, __dmul_rn(hq[q], V.v[q][i]));
+    w[i] = a;
+    if (partials) acc[0] = __dadd_rn(acc[0], __dmul_rn(a, a));
+  }
+  if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
+}
+
 // h[j+1][j] = ||w||, breakdown test, Givens update (solver.py:412-440).
 __global__ void finish_col_kernel(KState *st, int ld, int j, const double *partials,
                                   int n_partials, double tol) {
@@ -408,6 +694,88 @@ int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *v
   mgs_pass_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, l, j, w, vl, vl_scale, vn, vn_scale,
                                                      n, prev, n_prev, partials);
   PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int CNT>
+void dots_vec(const KState *st, const double *w, const double *vj, const MultiVec &V, int64_t n,
+              double *partials, cudaStream_t s) {
+  icwy_dots_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, w, vj, V, n, partials);
+}
+template <int CNT>
+void update_vec(const KState *st, int ld, int j, int i0, const MultiVec &V, double *w, int64_t n,
+                double *partials, cudaStream_t s) {
+  icwy_update_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, w, n,
+                                                                 partials);
+}
+
+#define PMK_CASES8(F) F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8)
+#define PMK_CASES16(F) PMK_CASES8(F) F(9) F(10) F(11) F(12) F(13) F(14) F(15) F(16)
+
+// Orthogonalise w against v[0..j] (ICWY form, see icwy_dots_vec_kernel) and
+// leave the partials of ||w||^2 in `norm_partials` (*n_norm of them).  All
+// passes use the fixed kRedBlocks grid (deterministic partial layout).
+int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
+                    const double *c0p, int n_c0, double *dot_partials, double *norm_partials,
+                    int *n_norm, cudaStream_t s) {
+  auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  bool vec = al(w);
+  for (int i = 0; i <= j; ++i) vec = vec && al(v[i]);
+  const int64_t gstride = (int64_t)(2 * kDotGroup + 1) * kRedBlocks;
+  for (int i0 = 0, gi = 0; i0 < j; i0 += kDotGroup, ++gi) {
+    const int cnt = (j - i0 < kDotGroup) ? j - i0 : kDotGroup;
+    MultiVec V{};
+    for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
+    prof::Scope scope(prof::kMGS, 8.0 * (cnt + 2) * (double)n, 4.0 * (2 * cnt + 1) * (double)n,
+                      s);
+    double *part = dot_partials + gi * gstride;
+    if (vec) {
+      switch (cnt) {
+#define PMK_DOTS_CASE(C)                        \
+  case C:                                       \
+    dots_vec<C>(st, w, v[j], V, n, part, s);    \
+    break;
+        PMK_CASES8(PMK_DOTS_CASE)
+#undef PMK_DOTS_CASE
+        default:
+          return PMK_ERR_ARG;
+      }
+    } else {
+      icwy_dots_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, w, v[j], V, cnt, n, part);
+    }
+    PMK_LAUNCH_CHECK();
+  }
+  {
+    prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
+    icwy_solve_kernel<<<1, 1024, (2 * j + 1) * sizeof(double), s>>>(st, ld, j, c0p, n_c0,
+                                                                   dot_partials, kRedBlocks);
+    PMK_LAUNCH_CHECK();
+  }
+  for (int i0 = 0; i0 <= j; i0 += kGroup) {
+    const int cnt = (j + 1 - i0 < kGroup) ? j + 1 - i0 : kGroup;
+    const bool last = i0 + cnt > j;
+    MultiVec V{};
+    for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
+    prof::Scope scope(prof::kMGS, 8.0 * (cnt + 2) * (double)n,
+                      2.0 * (cnt + (last ? 1 : 0)) * (double)n, s);
+    double *part = last ? norm_partials : nullptr;
+    if (vec) {
+      switch (cnt) {
+#define PMK_UPD_CASE(C)                                \
+  case C:                                              \
+    update_vec<C>(st, ld, j, i0, V, w, n, part, s);    \
+    break;
+        PMK_CASES16(PMK_UPD_CASE)
+#undef PMK_UPD_CASE
+        default:
+          return PMK_ERR_ARG;
+      }
+    } else {
+      icwy_update_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, cnt, w, n, part);
+    }
+    PMK_LAUNCH_CHECK();
+  }
+  *n_norm = kRedBlocks;
   return 0;
 }
 

@@ -15,6 +15,7 @@ struct KState {
   double *cs, *sn, *g, *y;
   double *vscale;  // vscale[l]: divisor of raw basis vector l (beta, h[l][l-1])
   double *hist;    // residual history rel_j
+  double *gram;    // cap x cap, row i = <v_i, v_l>, l < i (ICWY MGS)
   double beta, rel;
   int live;      // iterating (cleared on breakdown / convergence / beta == 0)
   int entered;   // parent was live when this invocation began
@@ -28,6 +29,17 @@ struct AssembleArgs {
   const double *v[kAsmChunk];  // normalised basis vectors
   const double *vt[kAsmChunk];
 };
+
+constexpr int kGroup = 16;     // basis vectors per ICWY update pass
+constexpr int kDotGroup = 8;   // basis vectors per ICWY dot pass (ptxas serialises
+                               // the loads of larger groups: ~3 TB/s at 12)
+struct MultiVec {
+  const double *v[kGroup];
+};
+// dot partial buffer: ceil(cap / kDotGroup) * (2 kDotGroup + 1) * kMaxPartials doubles
+int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
+                    const double *c0p, int n_c0, double *dot_partials, double *norm_partials,
+                    int *n_norm, cudaStream_t s);
 
 int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
                  cudaStream_t s);

@@ -95,7 +95,8 @@ __device__ __forceinline__ double stencil5(const Coef5 &a, bool hs, double vs, b
 
 struct TmaGeom {
   int single;  // 1: one column tile per row, box starts at x = 0
-  int tile_w;  // output columns per tile
+  int tile_w;  // output columns per tile (1-D: per segment)
+  int nseg;    // 1-D: column segments per row
   int gx, gy;  // column tiles, row groups
   int upc, n_chunks;
 };
@@ -334,6 +335,207 @@ __global__ void __launch_bounds__(kTmaThreads)
   }
 }
 
+// 1-D variant.  A 1-D slice is a single grid row, so one box per slice gave
+// each stage only ~200 outputs and the kernel was bound by per-stage
+// overhead.  Here a tile is up to R column segments of the row (each <= 252
+// columns + halo = one box, the segments of a tile are contiguous), a stage
+// holds the tile's boxes of one slice, and the 256 threads cover the tile's
+// outputs e = t + 256 u (column x0 + e; segment e / W, box offset e % W + 1).
+template <int MODE, int R, int S, bool VAR, bool GATHER, bool SCALED>
+__global__ void __launch_bounds__(kTmaThreads)
+    march_tma_1d_kernel(const MarchParams p, const __grid_constant__ CUtensorMap tm_v,
+                        const __grid_constant__ CUtensorMap tm_vt, const TmaGeom g) {
+  constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
+  constexpr int SL = (R * (kBox - 4) + kTmaThreads - 1) / kTmaThreads;  // outputs / thread
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double *smem = reinterpret_cast<double *>(
+      smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u));
+  __shared__ __align__(8) uint64_t bars[S];
+
+  if (!is_live(p.live)) return;
+  const int t = threadIdx.x;
+  if (t == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int nx = p.nx, m = p.m;  // m == nx
+  const int W = g.tile_w;
+  const int U = (MODE == kModeMVR) ? p.nu : 1;
+  const int n_units = p.n_steps / U + 1;
+  const int tiles = g.gx;
+  const int64_t n_items = (int64_t)tiles * g.n_chunks;
+  const double vsc = SCALED ? *p.v_scale : 1.0;
+  const bool fastdiv = SCALED && div_ok(vsc);
+  const double vrcp = fastdiv ? __drcp_rn(vsc) : 1.0;
+  double dot = 0.0;
+  uint32_t it = 0;
+
+  for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int tile = (int)(item % tiles);
+    const int chunk = (int)(item / tiles);
+    const int s0 = tile * R;
+    const int cnt = min(R, g.nseg - s0);  // segments (boxes) of this tile
+    const int x0 = s0 * W;                // first output column
+    const int cntW = min(cnt * W, nx - x0);
+    const int U0 = chunk * g.upc;
+    const int U1 = min(n_units, U0 + g.upc);
+    const int kb = (U0 == 0) ? 0 : U * (U0 - 1) + 1;
+    const int ke = U * (U1 - 1) + 1;
+    const int kstart = (kb > 0) ? kb - 1 : 0;
+    const int nsl = ke - kstart;
+    const int boxx = g.single ? 0 : x0 - 1;  // grid column of box 0's element 0
+    const int bo = g.single ? 0 : 1;         // box offset of a segment's first output
+    const uint32_t tx_bytes = (uint32_t)(NB * cnt * kBox * sizeof(double));
+
+    auto issue = [&](int k, int stage) {
+      double *sv = smem + (size_t)stage * NB * R * kBox;
+      mbar_expect_tx(&bars[stage], tx_bytes);
+      const int K = (k == 0) ? 0 : (k - 1) / p.nu + 1;
+      for (int r = 0; r < cnt; ++r) {
+        const int c = (int)((int64_t)k * m + boxx + r * W);
+        tma_row(sv + r * kBox, &tm_v, c & ~1, &bars[stage]);
+        if (NB == 2) {
+          const int cv = (int)((int64_t)K * p.m_coarse + boxx + r * W);
+          tma_row(sv + (R + r) * kBox, &tm_vt, cv & ~1, &bars[stage]);
+        }
+      }
+    };
+    if (t == 0) {
+      const int pre = nsl < S ? nsl : S;
+      for (int q = 0; q < pre; ++q) issue(kstart + q, (int)((it + q) % S));
+    }
+
+    // this thread's outputs: e = t + 256 u
+    int xs[SL], br[SL], bx[SL];
+    bool ok[SL];
+#pragma unroll
+    for (int u = 0; u < SL; ++u) {
+      const int e = t + u * kTmaThreads;
+      ok[u] = e < cntW;
+      xs[u] = x0 + e;
+      br[u] = ok[u] ? e / W : 0;
+      bx[u] = ok[u] ? e - br[u] * W + bo : 0;
+    }
+    double qprev[SL], acc[SL], v0next[SL];
+#pragma unroll
+    for (int u = 0; u < SL; ++u) qprev[u] = acc[u] = v0next[u] = 0.0;
+    Coef5 pcst, qcst;
+    if (!VAR) {
+      pcst = Coef5{p.P.c[0], p.P.c[1], p.P.c[2], p.P.c[3], p.P.c[4]};
+      qcst = Coef5{p.Q.c[0], p.Q.c[1], p.Q.c[2], p.Q.c[3], p.Q.c[4]};
+    }
+    const int nu = p.nu;
+    if (MODE == kModeIMV && p.partials) {
+      const int kf = (kb > kstart) ? kb : kstart;
+#pragma unroll
+      for (int u = 0; u < SL; ++u)
+        v0next[u] = (ok[u] && kf < ke) ? __ldg(p.v0 + (int64_t)kf * m + xs[u]) : 0.0;
+    }
+    for (int i = 0; i < nsl; ++i, ++it) {
+      const int k = kstart + i;
+      const bool prime = k < kb;
+      const int stage = (int)(it % S);
+      double *sv = smem + (size_t)stage * NB * R * kBox;
+      const int K = (k == 0) ? 0 : (k - 1) / nu + 1;
+      const int pos = (k == 0) ? nu - 1 : (k - 1) - (K - 1) * nu;
+      const bool drop = p.dropped && p.dropped[k];
+      const int pk = (int)(((int64_t)k * m + boxx) & 1);  // parity of box 0
+      const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
+      const int64_t kofs = (int64_t)k * m;
+      double v0v[SL];
+      if (MODE == kModeIMV && p.partials) {
+#pragma unroll
+        for (int u = 0; u < SL; ++u) v0v[u] = v0next[u];
+        const int kn = k + 1;
+        if (kn < ke) {
+#pragma unroll
+          for (int u = 0; u < SL; ++u)
+            if (ok[u]) v0next[u] = __ldg(p.v0 + (int64_t)kn * m + xs[u]);
+        }
+      }
+      mbar_wait(&bars[stage], (it / S) & 1);
+      // ---- pre-pass over the boxes' elements (v / scale or v - Z vt)
+      if (SCALED || MODE == kModeIMV) {
+        for (int r = 0; r < cnt; ++r) {
+          const int px = boxx + r * W + t;
+          if (t < kBox - 1 && px >= 0 && px < nx) {
+            double *cell = sv + r * kBox + t + ((pk + (r * W)) & 1);
+            double u = *cell;
+            if (SCALED && u != 0.0) u = fastdiv ? div_by(u, vsc, vrcp) : __ddiv_rn(u, vsc);
+            if (MODE == kModeIMV) {
+              const double z = GATHER
+                                    ? __ldg(p.vt + (int64_t)K * p.m_coarse + p.group_of[px])
+                                    : sv[(R + r) * kBox + t + ((pK + (r * W)) & 1)];
+              u = __dsub_rn(u, z);
+            }
+            *cell = u;
+          }
+        }
+        __syncthreads();
+      }
+      // ---- stencil (W, C, E in ascending column order; no S/N in 1-D)
+#pragma unroll
+      for (int u = 0; u < SL; ++u) {
+        if (!ok[u]) continue;
+        const int x = xs[u];
+        const double *row = sv + br[u] * kBox + ((pk + (br[u] * W)) & 1) + bx[u];
+        const double cur = row[0];
+        const double lf = (x > 0) ? row[-1] : 0.0;
+        const double rt = (x < nx - 1) ? row[1] : 0.0;
+        Coef5 a, b;
+        if (VAR) {
+          a = coef_at(p.P, x, m);
+          b = coef_at(p.Q, x, m);
+        } else {
+          a = pcst;
+          b = qcst;
+        }
+        const double Pu = __dadd_rn(
+            __dadd_rn(__dadd_rn(0.0, __dmul_rn(a.w, lf)), __dmul_rn(a.c, cur)), __dmul_rn(a.e, rt));
+        const double Qu = __dadd_rn(
+            __dadd_rn(__dadd_rn(0.0, __dmul_rn(b.w, lf)), __dmul_rn(b.c, cur)), __dmul_rn(b.e, rt));
+        if (!prime) {
+          double o;
+          if (k == 0) {
+            o = cur;  // identity block row (stepper.py:100)
+          } else {
+            o = __dsub_rn(Pu, qprev[u]);
+            if (drop) o = __dadd_rn(o, qprev[u]);  // stepper.py:103-104
+          }
+          if (MODE == kModeMV) {
+            p.out[kofs + x] = o;
+          } else if (MODE == kModeMVR) {
+            if (p.v_norm_out) p.v_norm_out[kofs + x] = cur;
+            const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));
+            if (p.inject) {
+              if (k % nu == 0) p.vh[(int64_t)(k / nu) * m + x] = sval;
+            } else {
+              acc[u] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[u], sval);
+              if (pos == nu - 1) p.vh[(int64_t)K * m + x] = acc[u];
+            }
+          } else {
+            if (p.x_out) p.x_out[kofs + x] = cur;
+            if (p.out) p.out[kofs + x] = o;
+            if (p.partials) dot = __dadd_rn(dot, __dmul_rn(o, v0v[u]));
+          }
+        }
+        qprev[u] = Qu;
+      }
+      __syncthreads();  // stage fully consumed
+      if (t == 0 && i + S < nsl) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(k + S, stage);
+      }
+    }
+  }
+  if (MODE == kModeIMV && p.partials) {
+    const double s = block_sum(dot);
+    if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
+  }
+}
+
 // ------------------------------------------------------------------ host
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
                                   const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
@@ -370,9 +572,10 @@ template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED>
 int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
             int *n_partials, double bytes, int cat) {
   constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
-  constexpr int ROWS = (DIM == 2) ? R + 2 : 1;
+  constexpr int ROWS = (DIM == 2) ? R + 2 : R;
   const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
-  auto kern = march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED>;
+  auto kern = (DIM == 2) ? march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED>
+                         : march_tma_1d_kernel<MODE, R, S, VAR, GATHER, SCALED>;
   static int occ = -1;
   if (occ < 0) {
     PMK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -382,8 +585,14 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
   }
   TmaGeom g;
   g.single = p.nx <= kBox - 1 ? 1 : 0;  // row + parity shift fits one box
-  g.tile_w = g.single ? p.nx : kBox - 4;  // halo + shift fit one box
-  g.gx = (p.nx + g.tile_w - 1) / g.tile_w;
+  if (g.single) {
+    g.tile_w = p.nx;
+  } else {  // halo + shift fit one box (<= 252); balance the tiles of a row
+    const int nt = (p.nx + (kBox - 4) - 1) / (kBox - 4);
+    g.tile_w = (p.nx + nt - 1) / nt;
+  }
+  g.nseg = (p.nx + g.tile_w - 1) / g.tile_w;
+  g.gx = (DIM == 2) ? g.nseg : (g.nseg + R - 1) / R;  // 1-D: R segments per tile
   g.gy = (DIM == 2) ? (p.ny + R - 1) / R : 1;
   const int U = (MODE == kModeMVR) ? p.nu : 1;
   const int n_units = p.n_steps / U + 1;
@@ -433,9 +642,9 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
   if (mode == kModeIMV && p.v0_scale) return 0;  // lazily scaled v_0: register path
   const bool var = p.P.var || p.Q.var;
   const bool d2 = p.ny > 1;
+  const bool wide1d = !d2 && p.nx > kBox - 1;  // 1-D rows of several segments
   const bool scaled = p.v_scale != nullptr;
   int rc = 0;
-  // R = 8 rows per tile in 2-D; S-stage rings sized for 2-3 CTAs per SM
 #define PMK_RUN(MODE, DIM, R, S, GATHER)                                                        \
   do {                                                                                         \
     if (var) {                                                                                 \
@@ -450,8 +659,11 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
                                                                    bytes, cat);                \
     }                                                                                          \
   } while (0)
-  // tile rows x ring stages per mode (tuning knob PMK_TMA_CFG=<mvr>,<imv>,
-  // each one of 0: 8x3/8x2, 1: 8x4/4x3, 2: 4x4/4x4, 3: 16x2/8x3)
+  // tile rows x ring stages per mode (tuning knob PMK_TMA_CFG=<mvr>,<imv>;
+  // mvr 0: 4x3, 1: 4x4, 2: 8x3, 3: 16x2; imv 0: 4x2, 1: 4x3, 2: 8x2, 3: 2x4).
+  // Defaults from an ncu sweep of the c5_c fine level (profiles/r1_march_sweep.md):
+  // 4-row tiles keep more CTAs resident, which hides the FP64 dependency
+  // chains better than taller tiles amortise the per-slice overhead.
   static int cfg_mvr = -1, cfg_imv = -1;
   if (cfg_mvr < 0) {
     cfg_mvr = 0;
@@ -460,16 +672,20 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
   }
   switch (mode) {
     case kModeMV:
-      if (d2) PMK_RUN(kModeMV, 2, 8, 3, false); else PMK_RUN(kModeMV, 1, 1, 8, false);
+      if (d2) PMK_RUN(kModeMV, 2, 8, 3, false);
+      else if (wide1d) PMK_RUN(kModeMV, 1, 8, 3, false);
+      else PMK_RUN(kModeMV, 1, 1, 8, false);
       break;
     case kModeMVR:
       if (d2) {
         switch (cfg_mvr) {
-          case 1: PMK_RUN(kModeMVR, 2, 8, 4, false); break;
-          case 2: PMK_RUN(kModeMVR, 2, 4, 4, false); break;
+          case 1: PMK_RUN(kModeMVR, 2, 4, 4, false); break;
+          case 2: PMK_RUN(kModeMVR, 2, 8, 3, false); break;
           case 3: PMK_RUN(kModeMVR, 2, 16, 2, false); break;
-          default: PMK_RUN(kModeMVR, 2, 8, 3, false);
+          default: PMK_RUN(kModeMVR, 2, 4, 3, false);
         }
+      } else if (wide1d) {
+        PMK_RUN(kModeMVR, 1, 8, 3, false);
       } else {
         PMK_RUN(kModeMVR, 1, 1, 8, false);
       }
@@ -477,15 +693,17 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
     case kModeIMV:
       if (d2) {
         if (gather) {
-          PMK_RUN(kModeIMV, 2, 8, 3, true);
+          PMK_RUN(kModeIMV, 2, 4, 3, true);
         } else {
           switch (cfg_imv) {
             case 1: PMK_RUN(kModeIMV, 2, 4, 3, false); break;
-            case 2: PMK_RUN(kModeIMV, 2, 4, 4, false); break;
-            case 3: PMK_RUN(kModeIMV, 2, 8, 3, false); break;
-            default: PMK_RUN(kModeIMV, 2, 8, 2, false);
+            case 2: PMK_RUN(kModeIMV, 2, 8, 2, false); break;
+            case 3: PMK_RUN(kModeIMV, 2, 2, 4, false); break;
+            default: PMK_RUN(kModeIMV, 2, 4, 2, false);
           }
         }
+      } else if (wide1d) {
+        if (gather) PMK_RUN(kModeIMV, 1, 8, 3, true); else PMK_RUN(kModeIMV, 1, 8, 3, false);
       } else {
         if (gather) PMK_RUN(kModeIMV, 1, 1, 8, true); else PMK_RUN(kModeIMV, 1, 1, 8, false);
       }

@@ -118,6 +118,12 @@ SMALL = {
     # 2-level TS family (build_two_level)
     "ts2_small": Case("ts2_small", 1, 31, 32, 0.5, 2, ("TS",), courant=0.64,
                       two_level_family="TS", max_outer=40),
+    # long 1-D horizon: the coarsest recurrence takes the chunked-scan path
+    # (>= 64 coarse slices, few modes); exact and decoupled (segment cuts)
+    "long1_small": Case("long1_small", 1, 31, 512, 0.5, 2, ("time",), courant=0.64,
+                        max_outer=40),
+    "long1_dec_small": Case("long1_dec_small", 1, 31, 512, 0.5, 2, ("time",), courant=0.64,
+                            n_cgs=6, max_outer=40),
     # 2-level MGRIT family (build_two_level; injection + ideal interpolation)
     "mgrit1_small": Case("mgrit1_small", 1, 31, 32, 0.5, 2, ("MGRIT",), nu=4, courant=0.64,
                          two_level_family="MGRIT", max_outer=40),

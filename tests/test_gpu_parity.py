@@ -180,7 +180,8 @@ def test_bad_shapes_raise():
 
 @pytest.mark.parametrize("dim,nx,ny,n_t,theta", [(1, 1023, 1, 16, 0.5), (2, 300, 20, 8, 0.5),
                                                  (2, 255, 9, 6, 1.0), (1, 255, 1, 12, 0.5),
-                                                 (2, 256, 5, 4, 0.5), (1, 17, 1, 9, 0.3)])
+                                                 (2, 256, 5, 4, 0.5), (1, 17, 1, 9, 0.3),
+                                                 (1, 700, 1, 10, 1.0), (2, 509, 7, 4, 0.5)])
 def test_fused_kernels_bitwise_wide_and_odd_grids(dim, nx, ny, n_t, theta):
     """K-MV, K-MVR (shift + restrict + normalised copy) and K-IMV against the
     oracle's operations, on grids wider than one 255-column tile and with odd
