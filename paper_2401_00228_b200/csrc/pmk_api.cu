@@ -178,10 +178,19 @@ MarchParams base_params(const pmk_level &L) {
   return p;
 }
 
+// PMK_MGS=classic: sequential MGS passes (bitwise the reference's Hessenberg)
+bool classic_mgs() {
+  static const bool on = [] {
+    const char *e = getenv("PMK_MGS");
+    return e && std::strcmp(e, "classic") == 0;
+  }();
+  return on;
+}
+
 // vh = Y^T (A v - mu v) ; optionally v_norm_out = v (normalised input)
 int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
            const double *v_scale, double *vh, double *scratch, double *v_norm_out,
-           const int *live, cudaStream_t s) {
+           const int *live, cudaStream_t s, bool exact = true) {
   MarchParams p = base_params(L);
   p.v = v;
   p.v_scale = v_scale;
@@ -189,6 +198,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   p.mu = mu;
   p.nu = P.nu;
   p.inject = P.mgrit ? 1 : 0;  // MgritPair.restrict (intergrid.py:152-155)
+  p.exact_scale = exact ? 1 : 0;
   const bool space = P.group_of != nullptr;
   PMK_RETURN_IF(space && !scratch, PMK_ERR_ARG);
   p.vh = space ? scratch : vh;
@@ -364,15 +374,6 @@ double *child_rhs(pmk_hier *H, int idx) {
   return H->lv[child].rhs;
 }
 
-// PMK_MGS=classic: sequential MGS passes (bitwise the reference's Hessenberg)
-bool classic_mgs() {
-  static const bool on = [] {
-    const char *e = getenv("PMK_MGS");
-    return e && std::strcmp(e, "classic") == 0;
-  }();
-  return on;
-}
-
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
                 cudaStream_t s) {
   LevelRT &R = H->lv[idx];
@@ -386,7 +387,10 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   const KState &K = R.h_state;
   // apply_preconditioner (solver.py:336-359); the pass that reads the
   // unnormalised basis vector also stores v_j = raw / scale.
-  int rc = do_mvr(R.L, R.P, H->mu, R.pending, K.vscale + j, vh, R.ts_scratch, v_out, live, s);
+  // (in-solver normalisation by reciprocal multiply, <= 1 ulp; the
+  // classic mode keeps the reference's division)
+  int rc = do_mvr(R.L, R.P, H->mu, R.pending, K.vscale + j, vh, R.ts_scratch, v_out, live, s,
+                  classic_mgs());
   if (rc) return rc;
   R.v.push_back(v_out);
   if (R.P.mgrit) {

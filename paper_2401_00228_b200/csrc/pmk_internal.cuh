@@ -152,6 +152,8 @@ struct MarchParams {
   double mu;
   int nu;
   int inject;          // MVR: MGRIT injection (vh_K = s_{nu K}) instead of the time sum
+  int exact_scale;     // v / *v_scale correctly rounded (register path); else the
+                       // TMA path multiplies by the rounded reciprocal (<= 1 ulp)
   double *vh;          // (n_T+1, m) time-summed (fine spatial)
   double *v_norm_out;  // optional: the normalised input v = v_raw / scale
   // IMV

@@ -3,11 +3,12 @@
 // (intergrid.py:51-63, 106-120).
 //
 // Krylov basis vectors: the reference appends b / beta and w / h[j+1, j]
-// (solver.py:395, 420).  Here the last MGS pass leaves w unnormalised and the
-// next iteration's K-MVR pass -- which reads it anyway -- divides by the norm
-// (IEEE division, bitwise the reference's values) and writes the normalised
-// v_j as a by-product (+8 B/unknown instead of a separate 16 B scale pass).
-// Every other reader (K-IMV, MGS, assembly) reads v_j division-free.
+// (solver.py:395, 420).  Here the last orthogonalisation pass leaves w
+// unnormalised and the next iteration's K-MVR pass -- which reads it anyway --
+// scales it (multiply by RN(1/h), within 1 ulp of the division; PMK_MGS=classic
+// divides exactly) and writes the normalised v_j as a by-product (+8 B/unknown
+// instead of a separate 16 B scale pass).  Every other reader (K-IMV, the
+// orthogonalisation, assembly) reads v_j scale-free.
 //
 // All reductions are two-level with a fixed grid (kRedBlocks) and a fixed
 // summation order, so results are bitwise reproducible.  The second level is

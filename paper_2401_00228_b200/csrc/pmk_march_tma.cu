@@ -18,7 +18,7 @@
 //
 // Compute per slice:
 //   pre-pass   each thread transforms one box column in place, once per
-//              element: v / scale (lazily normalised basis vector; the
+//              element: v * RN(1/scale) (lazily normalised basis vector; the
 //              normalised value is also stored, solver.py:395/420) or
 //              v - Z vt (K-IMV; vt staged through the same ring);
 //   stencil    each thread walks its column down the R rows keeping the
@@ -129,9 +129,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int n_units = p.n_steps / U + 1;
   const int tiles = g.gx * g.gy;
   const int64_t n_items = (int64_t)tiles * g.n_chunks;
-  const double vsc = SCALED ? *p.v_scale : 1.0;
-  const bool fastdiv = SCALED && div_ok(vsc);
-  const double vrcp = fastdiv ? __drcp_rn(vsc) : 1.0;
+  // normalisation of a lazily scaled basis vector: multiply by RN(1 / scale)
+  // (within 1 ulp of the division; exact_scale launches take the register path)
+  const double vrcp = SCALED ? __drcp_rn(*p.v_scale) : 1.0;
   double dot = 0.0;
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           double u = *cell;
           // 0 / scale = 0 (scale > 0): skipping it keeps exact zeros (the
           // first Krylov vector is mostly zero) off the division slow path
-          if (SCALED && u != 0.0) u = fastdiv ? div_by(u, vsc, vrcp) : __ddiv_rn(u, vsc);
+          if (SCALED) u = __dmul_rn(u, vrcp);
           if (MODE == kModeIMV) {
             const double z = GATHER ? __ldg(vtk + p.group_of[y * nx + px])
                                     : sv[(ROWS + r) * kBox + t + ((pK + (y & nx)) & 1)];
@@ -366,9 +366,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   const int n_units = p.n_steps / U + 1;
   const int tiles = g.gx;
   const int64_t n_items = (int64_t)tiles * g.n_chunks;
-  const double vsc = SCALED ? *p.v_scale : 1.0;
-  const bool fastdiv = SCALED && div_ok(vsc);
-  const double vrcp = fastdiv ? __drcp_rn(vsc) : 1.0;
+  // normalisation of a lazily scaled basis vector: multiply by RN(1 / scale)
+  // (within 1 ulp of the division; exact_scale launches take the register path)
+  const double vrcp = SCALED ? __drcp_rn(*p.v_scale) : 1.0;
   double dot = 0.0;
   uint32_t it = 0;
 
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           if (t < kBox - 1 && px >= 0 && px < nx) {
             double *cell = sv + r * kBox + t + ((pk + (r * W)) & 1);
             double u = *cell;
-            if (SCALED && u != 0.0) u = fastdiv ? div_by(u, vsc, vrcp) : __ddiv_rn(u, vsc);
+            if (SCALED) u = __dmul_rn(u, vrcp);
             if (MODE == kModeIMV) {
               const double z = GATHER
                                     ? __ldg(p.vt + (int64_t)K * p.m_coarse + p.group_of[px])
@@ -640,6 +640,7 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
     mvt = mv;
   }
   if (mode == kModeIMV && p.v0_scale) return 0;  // lazily scaled v_0: register path
+  if (p.v_scale && p.exact_scale) return 0;       // correctly rounded division
   const bool var = p.P.var || p.Q.var;
   const bool d2 = p.ny > 1;
   const bool wide1d = !d2 && p.nx > kBox - 1;  // 1-D rows of several segments

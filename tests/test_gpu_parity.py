@@ -121,6 +121,50 @@ def test_fgmres_internals_vs_oracle(name):
     assert rel(x.cpu().numpy(), xo) <= 1e-10
 
 
+_CLASSIC_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from tests.cases import SMALL, gpu_hierarchy, oracle_hierarchy
+from oracle import pintmk_oracle as O
+from paper_2401_00228_b200 import fgmres, multilevel_solve
+out = {}
+for name in ("c5_small", "mgrit2_small"):
+    case = SMALL[name]
+    h = gpu_hierarchy(case)
+    oh = oracle_hierarchy(case)
+    rhs = oh.rhs.ravel()
+    x, rep = fgmres(h, 0, rhs, tol=None, max_iter=3, keep_basis=True)
+    xo, info = O.fgmres(oh, 0, rhs, None, 3, keep_basis=True)
+    hd = np.abs(rep.metadata["hessenberg"] - info["hessenberg"]).max()
+    g = np.load(f"{sys.argv[1]}/tests/golden/{name}.npz")
+    xs, rs = multilevel_solve(gpu_hierarchy(case))
+    out[name] = {"hdiff": float(hd), "iters": rs.outer_iterations, "g_iters": int(g["iters"]),
+                 "xrel": float(np.linalg.norm(xs - g["x"]) / np.linalg.norm(g["x"]))}
+print(json.dumps(out))
+"""
+
+
+def test_classic_mgs_mode():
+    """PMK_MGS=classic (one basis vector per pass in the reference's order,
+    exact division for the normalised basis vectors) meets the same parity
+    bar as the default one-reduce orthogonalisation."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PMK_MGS="classic")
+    r = subprocess.run([sys.executable, "-c", _CLASSIC_SCRIPT, root], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, d in res.items():
+        assert d["hdiff"] <= 1e-12, (name, d)
+        assert abs(d["iters"] - d["g_iters"]) <= 1, (name, d)
+        assert d["xrel"] <= 1e-10, (name, d)
+
+
 def test_solve_is_deterministic():
     from paper_2401_00228_b200 import multilevel_solve
 
