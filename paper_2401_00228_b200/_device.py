@@ -31,10 +31,17 @@ class StencilTable:
     when X has entries outside the 5-point pattern of the grid."""
 
     def __init__(self, matrix: sp.spmatrix, nx: int, ny: int):
-        x = sp.csr_matrix(matrix)
         m = nx * ny
-        if x.shape != (m, m):
-            raise ValueError(f"operator shape {x.shape} does not match grid {nx}x{ny}")
+        if matrix.shape != (m, m):
+            raise ValueError(f"operator shape {matrix.shape} does not match grid {nx}x{ny}")
+        self.nx, self.ny, self.m = nx, ny, m
+        self._dev = None
+        self._coef = None
+        self._lazy = None
+        if sp.issparse(matrix) and matrix.format in ("csr", "csc") and \
+                self._from_full_pattern(matrix):
+            return
+        x = sp.csr_matrix(matrix)
         coo = x.tocoo()
         rows, cols, vals = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data
         off = cols - rows
@@ -55,14 +62,8 @@ class StencilTable:
         coef[slot, rows] = vals
         present = np.zeros((5, m), dtype=bool)
         present[slot, rows] = True
-        # geometric existence of each neighbour
-        iy, ix = np.divmod(np.arange(m), nx)
-        exists = np.stack([iy > 0, ix > 0, np.ones(m, bool), ix < nx - 1, iy < ny - 1])
-        if ny == 1:
-            exists[0] = False
-            exists[4] = False
-        self.nx, self.ny, self.m = nx, ny, m
-        self.coef = coef
+        exists = self._full_pattern(nx, ny)[4]
+        self._coef = coef
         constant = bool(np.all(present == exists))
         consts = np.zeros(5)
         if constant:
@@ -74,7 +75,90 @@ class StencilTable:
                 consts[s] = v[0] if v.size else 0.0
         self.constant = constant
         self.consts = consts
-        self._dev = None
+
+    @property
+    def coef(self) -> np.ndarray:
+        """(5, m) per-point coefficients (zeros where a neighbour is absent)."""
+        if self._coef is None:
+            self._coef = self._build_coef(*self._lazy)
+        return self._coef
+
+    # Fast path: the matrix (CSR, or CSC = the transpose of a CSR) has exactly
+    # the full 5-point pattern of the grid in canonical order (every pristine
+    # and time-coarsened level).  Its index arrays are compared with a cached
+    # pattern whose slot map is then reused; coefficients and constants are
+    # read from the matrix entries themselves.
+    _patterns: dict = {}
+    _OPP = (4, 3, 2, 1, 0)  # slot of the transposed entry: S<->N, W<->E
+
+    @classmethod
+    def _full_pattern(cls, nx: int, ny: int):
+        key = (nx, ny)
+        if key not in cls._patterns:
+            m = nx * ny
+            iy, ix = np.divmod(np.arange(m, dtype=np.int64), nx)
+            exists = np.stack([iy > 0, ix > 0, np.ones(m, bool), ix < nx - 1, iy < ny - 1])
+            if ny == 1:
+                exists[0] = False
+                exists[4] = False
+            offs = np.array([-nx, -1, 0, 1, nx], dtype=np.int64)
+            cols = np.arange(m, dtype=np.int64)[None, :] + offs[:, None]
+            # entries in row-major order, ascending column within a row
+            # (slots S < W < C < E < N)
+            mask_t = exists.T
+            indices = cols.T[mask_t]
+            slots = np.broadcast_to(np.arange(5), (m, 5))[mask_t]
+            rows = np.broadcast_to(np.arange(m, dtype=np.int64)[:, None], (m, 5))[mask_t]
+            indptr = np.concatenate([[0], np.cumsum(mask_t.sum(axis=1))])
+            by_slot = [np.flatnonzero(slots == s_) for s_ in range(5)]
+            cls._patterns[key] = (indptr, indices, slots, rows, exists, by_slot,
+                                  {np.dtype(np.int64): (indptr, indices),
+                                   np.dtype(np.int32): (indptr.astype(np.int32),
+                                                        indices.astype(np.int32))})
+        return cls._patterns[key]
+
+    def _from_full_pattern(self, x) -> bool:
+        nx, ny = self.nx, self.ny
+        if not x.has_sorted_indices:
+            return False
+        pat = self._full_pattern(nx, ny)
+        by_slot, typed = pat[5], pat[6]
+        ip, ix = typed.get(x.indices.dtype, typed[np.dtype(np.int64)])
+        if x.nnz != ix.size or not (np.array_equal(x.indptr, ip) and np.array_equal(x.indices, ix)):
+            return False
+        transposed = x.format == "csc"   # x = C^T, C the CSR with these arrays
+        data = x.data
+        # constant iff every entry equals the first entry of its slot
+        first = np.array([data[b[0]] if b.size else 0.0 for b in by_slot])
+        constant = bool(np.array_equal(data, first[pat[2]]))
+        consts = np.zeros(5)
+        if constant:
+            for s_ in range(5):
+                consts[self._OPP[s_] if transposed else s_] = first[s_]
+        self.constant = constant
+        self.consts = consts
+        self._lazy = (data.copy(), transposed)
+        return True
+
+    def _build_coef(self, data: np.ndarray, transposed: bool) -> np.ndarray:
+        nx, ny, m = self.nx, self.ny, self.m
+        _, _, slots, rows, exists = self._full_pattern(nx, ny)[:5]
+        c = np.zeros((5, m))
+        c[slots, rows] = data            # row form of C
+        if not transposed:
+            return c
+        # X = C^T: X[i, i + off_s] = C[i + off_s, i] = c[opp(s), i + off_s]
+        offs = (-nx, -1, 0, 1, nx)
+        out = np.zeros((5, m))
+        for s_ in range(5):
+            src = c[self._OPP[s_]]
+            o = offs[s_]
+            if o >= 0:
+                out[s_, :m - o] = src[o:]
+            else:
+                out[s_, -o:] = src[:m + o]
+            out[s_][~exists[s_]] = 0.0
+        return out
 
     def desc(self) -> _lib.Stencil:
         st = _lib.Stencil()

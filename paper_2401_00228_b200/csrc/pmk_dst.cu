@@ -228,10 +228,22 @@ __global__ void __launch_bounds__(32 * kDstWarps)
     const int x0 = (int)(item - k * xblocks) * kColTile;
     const int cw = min(kColTile, nx - x0);
     const double *src = in + k * m + x0;
-    __syncthreads();  // previous tile stored; tables loaded
-    for (int idx = threadIdx.x; idx < ny * kColTile; idx += blockDim.x) {
+    // stage the tile: all of a thread's loads issued before the first use
+    constexpr int kThreads = 32 * kDstWarps;
+    constexpr int ITEMS = (ny * kColTile + kThreads - 1) / kThreads;
+    double vals[ITEMS];
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int idx = threadIdx.x + u * kThreads;
       const int yy = idx / kColTile, c = idx - yy * kColTile;
-      tile[yy * TS + c] = (c < cw) ? __ldg(src + (int64_t)yy * nx + c) : 0.0;
+      vals[u] = (idx < ny * kColTile && c < cw) ? __ldg(src + (int64_t)yy * nx + c) : 0.0;
+    }
+    __syncthreads();  // previous tile stored; tables loaded
+#pragma unroll
+    for (int u = 0; u < ITEMS; ++u) {
+      const int idx = threadIdx.x + u * kThreads;
+      const int yy = idx / kColTile, c = idx - yy * kColTile;
+      if (idx < ny * kColTile) tile[yy * TS + c] = vals[u];
     }
     __syncthreads();
     for (int c0 = 0; c0 < cw; c0 += GROUPS) {

@@ -107,6 +107,18 @@ class Level:
         return (self.n_steps + 1) * self.state_dim
 
 
+_SOLVER_STREAMS: dict = {}
+
+
+def _solver_stream(device: int):
+    import torch
+
+    st = _SOLVER_STREAMS.get(device)
+    if st is None:
+        st = _SOLVER_STREAMS[device] = torch.cuda.Stream(device=device)
+    return st
+
+
 class LevelHierarchy:
     """Levels, fine system, config, and the native solver state."""
 
@@ -121,13 +133,16 @@ class LevelHierarchy:
 
     @contextlib.contextmanager
     def on_stream(self):
-        """Run on the hierarchy's own CUDA stream (the inner recursion is
+        """Run on the solver stream of the device (the inner recursion is
         replayed as CUDA graphs, which cannot be captured on the legacy
-        default stream); ordered after / before the caller's stream."""
+        default stream); ordered after / before the caller's stream.  One
+        stream per device for every hierarchy: torch's caching allocator
+        reuses a freed block only on the stream that freed it, so a stream
+        per hierarchy would strand every previous solve's memory."""
         import torch
 
         if self._stream is None:
-            self._stream = torch.cuda.Stream()
+            self._stream = _solver_stream(torch.cuda.current_device())
         caller = torch.cuda.current_stream()
         if caller == self._stream:
             yield
@@ -517,36 +532,48 @@ def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart:
     fine = hier.fine
     b = fine.rhs.reshape(-1)
     beta0 = _nrm2(b)
-    x = torch.zeros_like(b)
-    r = b.clone()
+    x = None          # x = 0 until the first cycle returns
+    r = b
+    rn = beta0
     hist: list[float] = []
     total = 0
     cycles = 0
     converged = False
+    final_rel = None
     while total < max_outer:
-        rn = _nrm2(r)
         if rn == 0.0:
             converged = True
+            final_rel = 0.0
             break
         m = min(restart, max_outer - total)
         dx, rep = _fgmres(hier, 0, r, tol=tol * beta0 / rn, max_iter=m)
-        x = x + dx
+        if x is None:
+            x = dx
+        else:
+            x.add_(dx)
+        del dx
         total += rep.outer_iterations
         cycles += 1
         hist += [h * rn / beta0 for h in rep.residual_history]
-        ax = torch.empty_like(b)
-        fine.matvec_into(x, ax)
-        r = b - ax
-        if _nrm2(r) / beta0 <= tol:
+        r = torch.empty_like(b)
+        fine.matvec_into(x, r)
+        torch.sub(b, r, out=r)     # r = b - A x
+        rn = _nrm2(r)
+        final_rel = rn / beta0     # ||b - A x|| / ||b|| (stepper.py:191-193)
+        if final_rel <= tol:
             converged = True
             break
         if rep.outer_iterations == 0:
             break
+    if x is None:
+        x = torch.zeros_like(b)
     report = SolveReport(method="fgmres[level 0]", tol=tol)
     report.outer_iterations = total
     report.residual_history = hist
     report.converged = converged
     report.metadata["restart_cycles"] = cycles
+    if final_rel is not None:
+        report.metadata["final_relative_residual"] = final_rel
     return x, report
 
 
@@ -576,7 +603,9 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     report.method = method_name
     report.wall_time = time.perf_counter() - t0
     report.tol = cfg.tol
-    true_res = hier.fine.relative_residual(x)
+    true_res = report.metadata.pop("final_relative_residual", None)
+    if true_res is None:
+        true_res = hier.fine.relative_residual(x)
     report.metadata["true_relative_residual"] = true_res
     report.converged = true_res <= cfg.tol
     report.level_stats = {"levels": hier.describe(), "moves": hier.moves}

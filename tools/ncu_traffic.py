@@ -11,16 +11,18 @@ import json
 import re
 import sys
 
-CATS = [("march_tma_kernel<0", "march_mv"), ("march_tma_kernel<1", "march_mvr"),
-        ("march_tma_kernel<2", "march_imv"), ("mgs_pass", "mgs_pass"),
-        ("dot_partials", "reduce"), ("diffsq_partials", "reduce"), ("assemble", "assemble"),
-        ("dst_rows", "coarse_gemm"), ("dst_cols", "coarse_gemm"), ("dgemm", "coarse_gemm"),
-        ("dst_recurrence", "coarse_recurrence"), ("copy_row", "coarse_misc")]
+CATS = [(r"march_tma(?:_1d)?_kernel<(?:\(int\))?0", "march_mv"),
+        (r"march_tma(?:_1d)?_kernel<(?:\(int\))?1", "march_mvr"),
+        (r"march_tma(?:_1d)?_kernel<(?:\(int\))?2", "march_imv"),
+        (r"mgs_pass|icwy_dots|icwy_update", "mgs_pass"),
+        (r"dot_partials|diffsq_partials", "reduce"), (r"assemble", "assemble"),
+        (r"dst_rows|dst_cols|dgemm", "coarse_gemm"),
+        (r"dst_recurrence|rec_chunk", "coarse_recurrence"), (r"copy_row", "coarse_misc")]
 
 
 def category(name: str):
     for key, cat in CATS:
-        if key in name:
+        if re.search(key, name):
             return cat
     return None
 
