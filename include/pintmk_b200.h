@@ -260,6 +260,14 @@ int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v,
 int pmk_profile_begin(int32_t with_events);
 int pmk_profile_end(double *stats, int32_t max_categories,
                     int32_t *n_categories);
+/* Same records split by attribution (phase ledger, parcost.py:63-122): rows
+ * of 7 doubles {level, hint, category, launches, total ms, bytes, flops},
+ * one per (level, hint, category) seen; level = the hierarchy level whose
+ * work issued the launch (-1: stand-alone call, n_levels-1: coarsest solve),
+ * hint = -1 none, 1 restriction, 2 interpolation (MGRIT ideal interpolation).
+ * Ends the profile like pmk_profile_end; PMK_ERR_ARG if max_rows is too
+ * small (*n_rows tells the size; the records are consumed either way). */
+int pmk_profile_end_levels(double *rows, int32_t max_rows, int32_t *n_rows);
 const char *pmk_profile_category(int32_t idx);
 int64_t pmk_launch_count(void);
 

@@ -18,4 +18,7 @@ from .solver import (Level, LevelHierarchy, SolveReport, SolverConfig,  # noqa: 
                      apply_preconditioner, build_hierarchy, build_two_level, fgmres,
                      multilevel_solve, two_level_solve)
 
+from .ledger import (PhaseLedger, measured_theta_scheme_ledger,  # noqa: F401
+                     report_relative)
+
 __version__ = "0.1.0"

@@ -89,6 +89,7 @@ SIGNATURES = {
                                            c_void_p]),
     "pmk_profile_begin": (c_int32, [c_int32]),
     "pmk_profile_end": (c_int32, [POINTER(c_double), c_int32, POINTER(c_int32)]),
+    "pmk_profile_end_levels": (c_int32, [POINTER(c_double), c_int32, POINTER(c_int32)]),
     "pmk_profile_category": (ctypes.c_char_p, [c_int32]),
     "pmk_launch_count": (c_int64, []),
     "pmk_div_check": (c_int32, [c_void_p, c_double, c_int64, c_void_p, c_void_p]),
@@ -173,6 +174,26 @@ def profile_end() -> dict:
         launches, ms, nbytes, flops = stats[4 * c: 4 * c + 4]
         if launches:
             out[name] = {"launches": int(launches), "ms": ms, "bytes": nbytes, "flops": flops}
+    return out
+
+
+HINTS = {-1: None, 1: "restriction", 2: "interpolation"}
+
+
+def profile_end_levels() -> list[dict]:
+    """Records since profile_begin split by attribution: a list of
+    {level, hint, category, launches, ms, bytes, flops} (synchronises)."""
+    lib = load()
+    cap = 512
+    rows = (c_double * (7 * cap))()
+    n = c_int32(0)
+    check(lib.pmk_profile_end_levels(rows, cap, ctypes.byref(n)), "profile_end_levels")
+    out = []
+    for i in range(n.value):
+        lvl, hint, cat, launches, ms, nbytes, flops = rows[7 * i: 7 * i + 7]
+        out.append({"level": int(lvl), "hint": HINTS.get(int(hint)),
+                    "category": lib.pmk_profile_category(int(cat)).decode(),
+                    "launches": int(launches), "ms": ms, "bytes": nbytes, "flops": flops})
     return out
 
 

@@ -21,6 +21,7 @@
 // launches of that invocation into no-ops.
 #include <cuda_runtime.h>
 
+#include <array>
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -38,10 +39,12 @@ using namespace pmk;
 // ------------------------------------------------------------- accounting
 namespace {
 struct ProfRec {
-  int cat;
+  int cat, level, hint;
   double bytes, flops;
   cudaEvent_t a, b;
 };
+thread_local int t_level = -1;  // level being issued (-1: stand-alone call)
+thread_local int t_hint = -1;
 std::atomic<int64_t> g_launches{0};
 std::mutex g_prof_mu;
 bool g_prof_on = false;
@@ -68,7 +71,7 @@ Scope::Scope(int cat, double bytes, double flops, cudaStream_t s) : rec(-1), str
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (!g_prof_on) return;
   std::lock_guard<std::mutex> g(g_prof_mu);
-  ProfRec r{cat, bytes, flops, pool_event(), pool_event()};
+  ProfRec r{cat, t_level, t_hint, bytes, flops, pool_event(), pool_event()};
   if (!r.a || !r.b) return;
   cudaEventRecord(r.a, s);
   rec = (int)g_recs.size();
@@ -78,6 +81,14 @@ Scope::~Scope() {
   if (rec < 0) return;
   std::lock_guard<std::mutex> g(g_prof_mu);
   cudaEventRecord(g_recs[rec].b, stream);
+}
+Tag::Tag(int level, int hint) : prev_level(t_level), prev_hint(t_hint) {
+  t_level = level;
+  t_hint = hint;
+}
+Tag::~Tag() {
+  t_level = prev_level;
+  t_hint = prev_hint;
 }
 }  // namespace prof
 }  // namespace pmk
@@ -205,7 +216,10 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   p.live = live;
   int rc = launch_march(kModeMVR, p, s, nullptr);
   if (rc) return rc;
-  if (space) return launch_ts_gather(P, scratch, vh, live, s);
+  if (space) {
+    prof::Tag tag(t_level, prof::kHintRestrict);
+    return launch_ts_gather(P, scratch, vh, live, s);
+  }
   return 0;
 }
 
@@ -282,6 +296,7 @@ inline const int *live_ptr(const LevelRT &R) { return &R.d_state->live; }
 
 int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double tol,
                  const int *parent_live, cudaStream_t s) {
+  prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
   PMK_RETURN_IF(!rhs || max_iter < 1, PMK_ERR_ARG);
@@ -362,6 +377,7 @@ int child_solve(pmk_hier *H, int idx, double *out, const int *live, cudaStream_t
   const int child = idx + 1;
   if (child == H->n_levels - 1) {
     PMK_RETURN_IF(!H->has_coarse || !H->coarse_rhs, PMK_ERR_STATE);
+    prof::Tag tag(child);
     return coarse_solve(H->coarse, H->coarse_rhs, out, live, s);
   }
   if (idx == 0) return fgmres_fixed_graph(H, child, out, live, s);
@@ -376,6 +392,7 @@ double *child_rhs(pmk_hier *H, int idx) {
 
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
                 cudaStream_t s) {
+  prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
   PMK_RETURN_IF(j != (int)R.vt.size() || j >= R.cap, PMK_ERR_STATE);
@@ -398,6 +415,7 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     // iteration's (fine-size) child_out (intergrid.py:157-167)
     rc = child_solve(H, idx, R.P.coarse_out, live, s);
     if (rc) return rc;
+    prof::Tag tag(idx, prof::kHintInterp);
     rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, live, s);
   } else {
     rc = child_solve(H, idx, child_out, live, s);
@@ -441,6 +459,7 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
 }
 
 int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
+  prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
   PMK_RETURN_IF(!x, PMK_ERR_ARG);
@@ -536,6 +555,39 @@ int pmk_profile_end(double *stats, int32_t max_categories, int32_t *n_categories
   g_recs.clear();
   g_pool_used = 0;
   if (n_categories) *n_categories = nc;
+  return 0;
+}
+
+int pmk_profile_end_levels(double *rows, int32_t max_rows, int32_t *n_rows) {
+  PMK_CUDA_TRY(cudaDeviceSynchronize());
+  std::lock_guard<std::mutex> g(g_prof_mu);
+  g_prof_on = false;
+  // aggregate by (level, hint, category), in order of first appearance
+  std::vector<std::array<double, 7>> agg;
+  std::unordered_map<int64_t, size_t> where;
+  for (const ProfRec &r : g_recs) {
+    float ms = 0.f;
+    PMK_CUDA_TRY(cudaEventElapsedTime(&ms, r.a, r.b));
+    const int64_t key = ((int64_t)(r.level + 1) << 32) | ((int64_t)(r.hint + 1) << 16) | r.cat;
+    auto it = where.find(key);
+    if (it == where.end()) {
+      it = where.emplace(key, agg.size()).first;
+      agg.push_back({(double)r.level, (double)r.hint, (double)r.cat, 0.0, 0.0, 0.0, 0.0});
+    }
+    auto &a = agg[it->second];
+    a[3] += 1.0;
+    a[4] += ms;
+    a[5] += r.bytes;
+    a[6] += r.flops;
+  }
+  g_recs.clear();
+  g_pool_used = 0;
+  const int n = (int)agg.size();
+  if (n_rows) *n_rows = n;
+  PMK_RETURN_IF(rows && n > max_rows, PMK_ERR_ARG);
+  if (rows)
+    for (int i = 0; i < n; ++i)
+      for (int c = 0; c < 7; ++c) rows[7 * i + c] = agg[i][c];
   return 0;
 }
 
@@ -758,11 +810,13 @@ int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v, double *
   cudaStream_t s = cs(stream);
   double *vh = child_rhs(H, idx);
   PMK_RETURN_IF(!vh, PMK_ERR_STATE);
+  prof::Tag tag(idx);
   int rc = do_mvr(R.L, R.P, H->mu, v, nullptr, vh, R.ts_scratch, nullptr, nullptr, s);
   if (rc) return rc;
   if (R.P.mgrit) {
     rc = child_solve(H, idx, R.P.coarse_out, nullptr, s);
     if (rc) return rc;
+    prof::Tag itag(idx, prof::kHintInterp);
     rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, nullptr, s);
   } else {
     rc = child_solve(H, idx, child_out, nullptr, s);

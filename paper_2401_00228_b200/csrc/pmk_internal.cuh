@@ -135,6 +135,14 @@ struct Scope {
   int rec;
   cudaStream_t stream;
 };
+// Attribution of recorded launches (phase ledger, reference parcost.py:63-122):
+// the hierarchy level whose work is being issued, and an optional phase hint.
+enum Hint { kHintNone = -1, kHintRestrict = 1, kHintInterp = 2 };
+struct Tag {
+  Tag(int level, int hint = kHintNone);
+  ~Tag();
+  int prev_level, prev_hint;
+};
 }  // namespace prof
 
 // ------------------------------------------------------------------ march

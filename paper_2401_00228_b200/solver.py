@@ -593,19 +593,34 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     cfg = hier.config
     rhs = hier.fine.rhs.reshape(-1)
     torch.cuda.synchronize()
+    if ledger is not None:  # real-time phase ledger (ledger.py): every launch timed
+        _lib.profile_begin(True)
     t0 = time.perf_counter()
-    with hier.on_stream():
-        if cfg.restart is None:
-            x, report = _fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer)
-        else:
-            x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart)
-    torch.cuda.synchronize()
-    report.method = method_name
-    report.wall_time = time.perf_counter() - t0
-    report.tol = cfg.tol
-    true_res = report.metadata.pop("final_relative_residual", None)
-    if true_res is None:
-        true_res = hier.fine.relative_residual(x)
+    try:
+        with hier.on_stream():
+            if cfg.restart is None:
+                x, report = _fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer)
+            else:
+                x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart)
+        torch.cuda.synchronize()
+        report.method = method_name
+        report.wall_time = time.perf_counter() - t0
+        report.tol = cfg.tol
+        true_res = report.metadata.pop("final_relative_residual", None)
+        if true_res is None:
+            true_res = hier.fine.relative_residual(x)
+    finally:
+        records = _lib.profile_end_levels() if ledger is not None else None
+    if ledger is not None:
+        from .ledger import charge_records, phase_of
+
+        charge_records(ledger, records)
+        report.simulated_elapsed = ledger.elapsed  # measured GPU microseconds
+        phase_ms: dict = {}
+        for r in records:
+            ph = "coarse_solve" if r["level"] >= 1 else phase_of(r)
+            phase_ms[ph] = phase_ms.get(ph, 0.0) + r["ms"]
+        report.metadata["gpu_phase_ms"] = phase_ms
     report.metadata["true_relative_residual"] = true_res
     report.converged = true_res <= cfg.tol
     report.level_stats = {"levels": hier.describe(), "moves": hier.moves}
