@@ -198,6 +198,11 @@ __global__ void __launch_bounds__(kTmaThreads)
     const int nu = p.nu;
     const int xo = x - boxx;         // box offset of this thread's output column
     const int gx0 = y0 * nx + x;     // in-slice index of (y0, x)
+    // Warps whose columns are all interior (no W/E boundary, all in range) on a
+    // tile whose rows and row neighbours all exist take the mask-free variant
+    // of the stencil pass below (same operations, no neighbour selects).
+    const bool tile_interior = DIM == 2 && (R % 2 == 0) && rlo == 0 && y0 + R <= ny - 1;
+    const bool warp_fast = __all_sync(0xffffffffu, tile_interior && xin && hw && he);
     double v0next[RO];
     if (MODE == kModeIMV && p.partials) {
       const int kf = (kb > kstart) ? kb : kstart;  // first non-prime slice
@@ -253,10 +258,69 @@ __global__ void __launch_bounds__(kTmaThreads)
         }
       }
       if (SCALED || MODE == kModeIMV) __syncthreads();
-      // ---- stencil pass down this thread's column.  Absent neighbours read
-      // as 0: adding their (+-0) products to the partial sum leaves it
-      // unchanged, so the sum equals the reference's sparse product.
-      if (xin) {
+      // ---- stencil pass, mask-free variant: every neighbour exists, k >= 1,
+      // no dropped coupling.  Tile rows start at even y0 (R even) and box row
+      // r holds grid row y0 - 1 + r, odd for even r: its parity shift
+      // (pk + y nx) & 1 is pk ^ (nx & 1) on even box rows and pk on odd ones.
+      if (warp_fast && k > 0 && !drop) {
+        const int sh0 = pk ^ (nx & 1), sh1 = pk;  // box rows 0, 2, ... / 1, 3, ...
+        const double *col = sv + xo;
+        double up = col[sh0];
+        double cur = col[kBox + sh1];
+        const bool wn = MODE == kModeMVR && p.v_norm_out != nullptr;
+        const bool inj = MODE == kModeMVR && p.inject;
+        const bool closes = pos == nu - 1, opens = pos == 0;
+#pragma unroll
+        for (int r = 0; r < RO; ++r) {
+          const double *row = col + (r + 1) * kBox + (((r + 1) & 1) ? sh1 : sh0);
+          const double dn = col[(r + 2) * kBox + (((r + 2) & 1) ? sh1 : sh0)];
+          const double lf = row[-1], rt = row[1];
+          Coef5 a, b;
+          if (VAR) {
+            a = coef_at(p.P, gx0 + r * nx, m);
+            b = coef_at(p.Q, gx0 + r * nx, m);
+          } else {
+            a = pcst;
+            b = qcst;
+          }
+          const double Pu = __dadd_rn(
+              __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a.s, up), __dmul_rn(a.w, lf)),
+                                  __dmul_rn(a.c, cur)),
+                        __dmul_rn(a.e, rt)),
+              __dmul_rn(a.n, dn));
+          const double Qu = __dadd_rn(
+              __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(b.s, up), __dmul_rn(b.w, lf)),
+                                  __dmul_rn(b.c, cur)),
+                        __dmul_rn(b.e, rt)),
+              __dmul_rn(b.n, dn));
+          if (!prime) {
+            const double o = __dsub_rn(Pu, qprev[r]);
+            const int64_t gi = kofs + gx0 + r * nx;
+            if (MODE == kModeMV) {
+              p.out[gi] = o;
+            } else if (MODE == kModeMVR) {
+              if (wn) p.v_norm_out[gi] = cur;
+              const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
+              if (inj) {
+                if (k % nu == 0) p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sval;
+              } else {
+                acc[r] = opens ? sval : __dadd_rn(acc[r], sval);
+                if (closes) p.vh[(int64_t)K * m + gx0 + r * nx] = acc[r];
+              }
+            } else {
+              if (p.x_out) p.x_out[gi] = cur;
+              if (p.out) p.out[gi] = o;
+              if (p.partials) dot = __dadd_rn(dot, __dmul_rn(o, v0v[r]));
+            }
+          }
+          qprev[r] = Qu;
+          up = cur;
+          cur = dn;
+        }
+      } else if (xin) {
+        // ---- generic variant.  Absent neighbours read as 0: adding their
+        // (+-0) products to the partial sum leaves it unchanged, so the sum
+        // equals the reference's sparse product.
         const double *col = sv + xo;
         double up = (DIM == 2 && rlo == 0) ? col[(pk + ((y0 - 1) & nx)) & 1] : 0.0;
         double cur = col[((DIM == 2) ? kBox : 0) + ((pk + (y0 & nx)) & 1)];
