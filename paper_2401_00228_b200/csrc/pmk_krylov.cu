@@ -578,6 +578,67 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Same sum for a time-only coarse mapping with nu = 2 (group_of == nullptr),
+// for the few-vector assemblies of the inner levels; templated on the
+// vector count.  Grid y runs over coarse slices K: a block owns the fine
+// slices of K (slice 0 alone for K = 0, else 2K-1 and 2K), and each thread
+// loads, for U elements of the slice, the coarse value vt_q once and both
+// fine values v_q up front (3 U CNT loads in flight), so every coarse value
+// is read once and no load waits behind a store.
+template <int CNT>
+__global__ void __launch_bounds__(256)
+    assemble_pair_kernel(const KState *st, AssembleArgs a, double *x, int rows, int m,
+                         int first) {
+  if (!st->entered) return;
+  constexpr int U = (12 / (3 * CNT)) > 1 ? 12 / (3 * CNT) : 1;
+  const int n_iter = st->n_iter;
+  if (first > 0 && first >= n_iter) return;
+  const int hi = min(n_iter, first + CNT);
+  double y[CNT];
+#pragma unroll
+  for (int q = 0; q < CNT; ++q) y[q] = (first + q < hi) ? st->y[first + q] : 0.0;
+  const int chunk = 256 * U;
+  const int n_coarse = (rows - 1) / 2 + 1;
+  for (int K = blockIdx.y; K < n_coarse; K += gridDim.y) {
+    const int64_t cbase = (int64_t)K * m;
+    const int k0 = (K == 0) ? 0 : 2 * K - 1;
+    const bool two = K > 0;
+    for (int i0 = blockIdx.x * chunk; i0 < m; i0 += gridDim.x * chunk) {
+      double tt[U][CNT], v0[U][CNT], v1[U][CNT], a0[U], a1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + threadIdx.x + u * 256;
+        const bool ok = i < m;
+        const int64_t e0 = (int64_t)k0 * m + i, e1 = e0 + m;
+        a0[u] = (first == 0 || !ok) ? 0.0 : x[e0];
+        a1[u] = (first == 0 || !ok || !two) ? 0.0 : x[e1];
+#pragma unroll
+        for (int q = 0; q < CNT; ++q) {
+          const bool on = ok && first + q < hi;
+          tt[u][q] = on ? __ldg(a.vt[q] + cbase + i) : 0.0;
+          v0[u][q] = on ? __ldg(a.v[q] + e0) : 0.0;
+          v1[u][q] = (on && two) ? __ldg(a.v[q] + e1) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + threadIdx.x + u * 256;
+        if (i >= m) continue;
+        const int64_t e0 = (int64_t)k0 * m + i;
+        double s0 = a0[u], s1 = a1[u];
+#pragma unroll
+        for (int q = 0; q < CNT; ++q)
+          if (first + q < hi) {
+            s0 = __dadd_rn(s0, __dmul_rn(y[q], __dsub_rn(v0[u][q], tt[u][q])));
+            s1 = __dadd_rn(s1, __dmul_rn(y[q], __dsub_rn(v1[u][q], tt[u][q])));
+          }
+        x[e0] = s0;
+        if (two) x[e0 + m] = s1;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------- transfers
 __global__ void restrict_time_kernel(const double *v, double *vh, int nu, int n_T, int m) {
   const int64_t total = (int64_t)(n_T + 1) * m;
@@ -802,6 +863,26 @@ int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t 
                     a.count * (8.0 * (double)n + 8.0 * nc * m_coarse) + (first ? 16.0 : 8.0) * n,
                     0.0, s);
   const int rows = (int)(n / m);
+  if (!group_of && nu == 2 && m_coarse == m && a.count >= 1 && a.count <= 8) {
+    const int u = (12 / (3 * a.count)) > 1 ? 12 / (3 * a.count) : 1;
+    const int xb = (m + 256 * u - 1) / (256 * u);
+    const int target = 8 * kSMs * 8;  // ~8 waves of 8 resident blocks per SM
+    const int n_coarse = (rows - 1) / 2 + 1;
+    int yb = (target + xb - 1) / xb;
+    if (yb > n_coarse) yb = n_coarse;
+    dim3 grid(xb, yb < 1 ? 1 : yb);
+    switch (a.count) {
+#define PMK_ASM_CASE(C)                                                             \
+  case C:                                                                           \
+    assemble_pair_kernel<C><<<grid, 256, 0, s>>>(st, a, x, rows, m, first);         \
+    break;
+      PMK_ASM_CASE(1) PMK_ASM_CASE(2) PMK_ASM_CASE(3) PMK_ASM_CASE(4)
+      PMK_ASM_CASE(5) PMK_ASM_CASE(6) PMK_ASM_CASE(7) PMK_ASM_CASE(8)
+#undef PMK_ASM_CASE
+    }
+    PMK_LAUNCH_CHECK();
+    return 0;
+  }
   dim3 grid((m + 255) / 256, rows < 1024 ? rows : 1024);
   if (grid.x > 64) grid.x = 64;
   assemble_kernel<<<grid, 256, 0, s>>>(st, a, x, rows, m, nu, m_coarse, group_of, first);
