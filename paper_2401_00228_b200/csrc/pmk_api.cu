@@ -113,6 +113,10 @@ struct LevelRT {
   int cap = 0;
   double *partA = nullptr, *partB = nullptr;
   double *partM = nullptr;  // ICWY dot partials
+  // ||rhs||^2 partials left by the parent's K-MVR for the next begin (inner
+  // levels; rhs_part_n = 0: none, begin computes the norm itself)
+  double *rhs_part = nullptr;
+  int rhs_part_n = 0;
   double tol = 0.0;
   // CUDA graphs of this level's inner solve, keyed by its output buffer
   std::unordered_set<const double *> seen;
@@ -189,6 +193,11 @@ MarchParams base_params(const pmk_level &L) {
   return p;
 }
 
+// K-MVR of level idx into the child's rhs; when the child is an inner FGMRES
+// level its ||rhs||^2 partials come out of the same pass.
+int mvr_into_child(pmk_hier *H, int idx, const double *v, const double *v_scale,
+                   double *v_norm_out, const int *live, cudaStream_t s, bool exact);
+
 // PMK_MGS=classic: sequential MGS passes (bitwise the reference's Hessenberg)
 bool classic_mgs() {
   static const bool on = [] {
@@ -201,7 +210,8 @@ bool classic_mgs() {
 // vh = Y^T (A v - mu v) ; optionally v_norm_out = v (normalised input)
 int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
            const double *v_scale, double *vh, double *scratch, double *v_norm_out,
-           const int *live, cudaStream_t s, bool exact = true) {
+           const int *live, cudaStream_t s, bool exact = true, double *vh_partials = nullptr,
+           int *n_vh = nullptr) {
   MarchParams p = base_params(L);
   p.v = v;
   p.v_scale = v_scale;
@@ -214,7 +224,10 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   PMK_RETURN_IF(space && !scratch, PMK_ERR_ARG);
   p.vh = space ? scratch : vh;
   p.live = live;
-  int rc = launch_march(kModeMVR, p, s, nullptr);
+  p.vh_partials = space ? nullptr : vh_partials;  // a space pair gathers afterwards
+  int np = 0;
+  int rc = launch_march(kModeMVR, p, s, &np);
+  if (n_vh) *n_vh = p.vh_partials ? np : 0;
   if (rc) return rc;
   if (space) {
     prof::Tag tag(t_level, prof::kHintRestrict);
@@ -304,9 +317,15 @@ int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double t
   if (rc) return rc;
   R.tol = tol;
   R.parent_live = parent_live;
-  rc = launch_dot_partials(rhs, nullptr, rhs, nullptr, R.N, R.partA, parent_live, s);
-  if (rc) return rc;
-  rc = launch_begin(R.d_state, R.partA, kRedBlocks, parent_live, s);
+  if (R.rhs_part_n > 0 && rhs == R.rhs) {
+    // ||rhs||^2 partials produced by the parent's K-MVR while writing rhs
+    rc = launch_begin(R.d_state, R.rhs_part, R.rhs_part_n, parent_live, s);
+    R.rhs_part_n = 0;
+  } else {
+    rc = launch_dot_partials(rhs, nullptr, rhs, nullptr, R.N, R.partA, parent_live, s);
+    if (rc) return rc;
+    rc = launch_begin(R.d_state, R.partA, kRedBlocks, parent_live, s);
+  }
   if (rc) return rc;
   R.rhs_cur = rhs;
   R.pending = rhs;
@@ -390,6 +409,21 @@ double *child_rhs(pmk_hier *H, int idx) {
   return H->lv[child].rhs;
 }
 
+int mvr_into_child(pmk_hier *H, int idx, const double *v, const double *v_scale,
+                   double *v_norm_out, const int *live, cudaStream_t s, bool exact) {
+  LevelRT &R = H->lv[idx];
+  double *vh = child_rhs(H, idx);
+  PMK_RETURN_IF(!vh, PMK_ERR_STATE);
+  const int child = idx + 1;
+  LevelRT *C = (child < H->n_levels - 1) ? &H->lv[child] : nullptr;
+  double *part = (C && C->rhs_part) ? C->rhs_part : nullptr;
+  int n = 0;
+  const int rc = do_mvr(R.L, R.P, H->mu, v, v_scale, vh, R.ts_scratch, v_norm_out, live, s,
+                        exact, part, &n);
+  if (C) C->rhs_part_n = part ? n : 0;
+  return rc;
+}
+
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
                 cudaStream_t s) {
   prof::Tag tag(idx);
@@ -406,8 +440,7 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   // unnormalised basis vector also stores v_j = raw / scale.
   // (in-solver normalisation by reciprocal multiply, <= 1 ulp; the
   // classic mode keeps the reference's division)
-  int rc = do_mvr(R.L, R.P, H->mu, R.pending, K.vscale + j, vh, R.ts_scratch, v_out, live, s,
-                  classic_mgs());
+  int rc = mvr_into_child(H, idx, R.pending, K.vscale + j, v_out, live, s, classic_mgs());
   if (rc) return rc;
   R.v.push_back(v_out);
   if (R.P.mgrit) {
@@ -701,6 +734,7 @@ void pmk_hier_destroy(pmk_hier *H) {
   for (auto &R : H->lv) {
     for (auto &kv : R.graphs) cudaGraphExecDestroy(kv.second.first);
     if (R.d_block) cudaFree(R.d_block);
+    if (R.rhs_part) cudaFree(R.rhs_part);
   }
   delete H;
 }
@@ -746,6 +780,9 @@ int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *v
   PMK_RETURN_IF(R.P.group_of && !ts_scratch, PMK_ERR_ARG);
   R.rhs = rhs;
   R.w_buf = w_buf;
+  if (idx > 0 && !R.rhs_part)  // the parent's K-MVR leaves ||rhs||^2 partials here
+    PMK_CUDA_TRY(cudaMalloc(&R.rhs_part, kMaxPartials * sizeof(double)));
+  R.rhs_part_n = 0;
   R.v_slots.assign(v_slots, v_slots + n_slots);
   R.child_out.assign(child_out, child_out + n_slots);
   R.ts_scratch = ts_scratch;
@@ -811,7 +848,7 @@ int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v, double *
   double *vh = child_rhs(H, idx);
   PMK_RETURN_IF(!vh, PMK_ERR_STATE);
   prof::Tag tag(idx);
-  int rc = do_mvr(R.L, R.P, H->mu, v, nullptr, vh, R.ts_scratch, nullptr, nullptr, s);
+  int rc = mvr_into_child(H, idx, v, nullptr, nullptr, nullptr, s, true);
   if (rc) return rc;
   if (R.P.mgrit) {
     rc = child_solve(H, idx, R.P.coarse_out, nullptr, s);

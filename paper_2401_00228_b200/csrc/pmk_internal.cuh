@@ -163,6 +163,8 @@ struct MarchParams {
   int exact_scale;     // v / *v_scale correctly rounded (register path); else the
                        // TMA path multiplies by the rounded reciprocal (<= 1 ulp)
   double *vh;          // (n_T+1, m) time-summed (fine spatial)
+  double *vh_partials; // optional: per-block partial sums of vh^2 (TMA path only;
+                       // launch_march reports 0 partials when it is not produced)
   double *v_norm_out;  // optional: the normalised input v = v_raw / scale
   // IMV
   const double *vt;

@@ -290,8 +290,13 @@ int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials
   switch (mode) {
     case kModeMV:
       return dispatch<kModeMV>(p, s, n_partials, bytes, cat);
-    case kModeMVR:
-      return dispatch<kModeMVR>(p, s, n_partials, bytes, cat);
+    case kModeMVR: {
+      MarchParams q = p;
+      q.vh_partials = nullptr;  // ||vh||^2 partials are a TMA-path product
+      const int rc = dispatch<kModeMVR>(q, s, nullptr, bytes, cat);
+      if (n_partials) *n_partials = 0;
+      return rc;
+    }
     default:
       return dispatch<kModeIMV>(p, s, n_partials, bytes, cat);
   }

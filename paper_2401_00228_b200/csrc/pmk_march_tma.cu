@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   // (within 1 ulp of the division; exact_scale launches take the register path)
   const double vrcp = SCALED ? __drcp_rn(*p.v_scale) : 1.0;
   double dot = 0.0;
+  double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -302,10 +303,16 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (wn) p.v_norm_out[gi] = cur;
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
               if (inj) {
-                if (k % nu == 0) p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sval;
+                if (k % nu == 0) {
+                  p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sval;
+                  vsq = __dadd_rn(vsq, __dmul_rn(sval, sval));
+                }
               } else {
                 acc[r] = opens ? sval : __dadd_rn(acc[r], sval);
-                if (closes) p.vh[(int64_t)K * m + gx0 + r * nx] = acc[r];
+                if (closes) {
+                  p.vh[(int64_t)K * m + gx0 + r * nx] = acc[r];
+                  vsq = __dadd_rn(vsq, __dmul_rn(acc[r], acc[r]));
+                }
               }
             } else {
               if (p.x_out) p.x_out[gi] = cur;
@@ -368,10 +375,16 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (p.v_norm_out) p.v_norm_out[kofs + gi] = cur;
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
               if (p.inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
-                if (k % nu == 0) p.vh[(int64_t)(k / nu) * m + gi] = sval;
+                if (k % nu == 0) {
+                  p.vh[(int64_t)(k / nu) * m + gi] = sval;
+                  vsq = __dadd_rn(vsq, __dmul_rn(sval, sval));
+                }
               } else {
                 acc[r] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[r], sval);
-                if (pos == nu - 1) p.vh[(int64_t)K * m + gi] = acc[r];
+                if (pos == nu - 1) {
+                  p.vh[(int64_t)K * m + gi] = acc[r];
+                  vsq = __dadd_rn(vsq, __dmul_rn(acc[r], acc[r]));
+                }
               }
             } else {
               if (p.x_out) p.x_out[kofs + gi] = cur;
@@ -396,6 +409,10 @@ __global__ void __launch_bounds__(kTmaThreads)
   if (MODE == kModeIMV && p.partials) {
     const double s = block_sum(dot);
     if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
+  }
+  if (MODE == kModeMVR && p.vh_partials) {
+    const double s = block_sum(vsq);
+    if (threadIdx.x == 0) p.vh_partials[blockIdx.x] = s;
   }
 }
 
@@ -434,6 +451,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   // (within 1 ulp of the division; exact_scale launches take the register path)
   const double vrcp = SCALED ? __drcp_rn(*p.v_scale) : 1.0;
   double dot = 0.0;
+  double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;
 
   for (int64_t item = blockIdx.x; item < n_items; item += gridDim.x) {
@@ -574,10 +592,16 @@ __global__ void __launch_bounds__(kTmaThreads)
             if (p.v_norm_out) p.v_norm_out[kofs + x] = cur;
             const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));
             if (p.inject) {
-              if (k % nu == 0) p.vh[(int64_t)(k / nu) * m + x] = sval;
+              if (k % nu == 0) {
+                p.vh[(int64_t)(k / nu) * m + x] = sval;
+                vsq = __dadd_rn(vsq, __dmul_rn(sval, sval));
+              }
             } else {
               acc[u] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[u], sval);
-              if (pos == nu - 1) p.vh[(int64_t)K * m + x] = acc[u];
+              if (pos == nu - 1) {
+                p.vh[(int64_t)K * m + x] = acc[u];
+                vsq = __dadd_rn(vsq, __dmul_rn(acc[u], acc[u]));
+              }
             }
           } else {
             if (p.x_out) p.x_out[kofs + x] = cur;
@@ -597,6 +621,10 @@ __global__ void __launch_bounds__(kTmaThreads)
   if (MODE == kModeIMV && p.partials) {
     const double s = block_sum(dot);
     if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
+  }
+  if (MODE == kModeMVR && p.vh_partials) {
+    const double s = block_sum(vsq);
+    if (threadIdx.x == 0) p.vh_partials[blockIdx.x] = s;
   }
 }
 
@@ -662,7 +690,7 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
   const int n_units = p.n_steps / U + 1;
   const int tiles = g.gx * g.gy;
   int grid_cap = occ * kSMs;
-  if (MODE == kModeIMV && grid_cap > kMaxPartials) grid_cap = kMaxPartials;
+  if (MODE != kModeMV && grid_cap > kMaxPartials) grid_cap = kMaxPartials;  // partials
   // ~8 work items per resident CTA; chunks of at most 32 units (one extra
   // prime slice per chunk, served from L2).
   int64_t upc = ((int64_t)n_units * tiles) / (8LL * grid_cap);
