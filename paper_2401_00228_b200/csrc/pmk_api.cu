@@ -220,6 +220,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   p.nu = P.nu;
   p.inject = P.mgrit ? 1 : 0;  // MgritPair.restrict (intergrid.py:152-155)
   p.exact_scale = exact ? 1 : 0;
+  p.fma = exact ? 0 : 1;  // in-solver (non-exact) passes may fuse
   const bool space = P.group_of != nullptr;
   PMK_RETURN_IF(space && !scratch, PMK_ERR_ARG);
   p.vh = space ? scratch : vh;
@@ -240,8 +241,10 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
 // already interpolated fine vector (identity coarse mapping).
 int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double *v_scale,
            const double *vt, double *x, double *w, const double *v0, const double *v0_scale,
-           double *partials, int *n_partials, const int *live, cudaStream_t s) {
+           double *partials, int *n_partials, const int *live, cudaStream_t s,
+           bool fused = false) {
   MarchParams p = base_params(L);
+  p.fma = fused ? 1 : 0;
   p.v = v;
   p.v_scale = v_scale;
   p.nu = P.mgrit ? 1 : P.nu;
@@ -457,7 +460,7 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407)
   int np = 0;
   rc = do_imv(R.L, R.P, v_out, nullptr, child_out, nullptr, w_next, R.v[0], nullptr, R.partA,
-              &np, live, s);
+              &np, live, s, !classic_mgs());
   if (rc) return rc;
   if (!classic_mgs()) {
     // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412)

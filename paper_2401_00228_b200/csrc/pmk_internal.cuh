@@ -162,6 +162,8 @@ struct MarchParams {
   int inject;          // MVR: MGRIT injection (vh_K = s_{nu K}) instead of the time sum
   int exact_scale;     // v / *v_scale correctly rounded (register path); else the
                        // TMA path multiplies by the rounded reciprocal (<= 1 ulp)
+  int fma;             // in-solver passes: the stencil sums, shift and dot may use
+                       // fused multiply-add (off: bitwise the reference's product)
   double *vh;          // (n_T+1, m) time-summed (fine spatial)
   double *vh_partials; // optional: per-block partial sums of vh^2 (TMA path only;
                        // launch_march reports 0 partials when it is not produced)

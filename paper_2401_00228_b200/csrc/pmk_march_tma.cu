@@ -101,7 +101,7 @@ struct TmaGeom {
   int upc, n_chunks;
 };
 
-template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED>
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA>
 __global__ void __launch_bounds__(kTmaThreads)
     march_tma_kernel(const MarchParams p, const __grid_constant__ CUtensorMap tm_v,
                      const __grid_constant__ CUtensorMap tm_vt, const TmaGeom g) {
@@ -284,16 +284,20 @@ __global__ void __launch_bounds__(kTmaThreads)
             a = pcst;
             b = qcst;
           }
-          const double Pu = __dadd_rn(
-              __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a.s, up), __dmul_rn(a.w, lf)),
-                                  __dmul_rn(a.c, cur)),
-                        __dmul_rn(a.e, rt)),
-              __dmul_rn(a.n, dn));
-          const double Qu = __dadd_rn(
-              __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(b.s, up), __dmul_rn(b.w, lf)),
-                                  __dmul_rn(b.c, cur)),
-                        __dmul_rn(b.e, rt)),
-              __dmul_rn(b.n, dn));
+          double Pu, Qu;
+          if (FMA) {  // in-solver passes: fused, same ascending column order
+            Pu = fma(a.n, dn, fma(a.e, rt, fma(a.c, cur, fma(a.w, lf, __dmul_rn(a.s, up)))));
+            Qu = fma(b.n, dn, fma(b.e, rt, fma(b.c, cur, fma(b.w, lf, __dmul_rn(b.s, up)))));
+          } else {  // separately rounded: bitwise the reference's sparse product
+            Pu = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a.s, up), __dmul_rn(a.w, lf)),
+                                               __dmul_rn(a.c, cur)),
+                                     __dmul_rn(a.e, rt)),
+                           __dmul_rn(a.n, dn));
+            Qu = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(b.s, up), __dmul_rn(b.w, lf)),
+                                               __dmul_rn(b.c, cur)),
+                                     __dmul_rn(b.e, rt)),
+                           __dmul_rn(b.n, dn));
+          }
           if (!prime) {
             const double o = __dsub_rn(Pu, qprev[r]);
             const int64_t gi = kofs + gx0 + r * nx;
@@ -301,7 +305,7 @@ __global__ void __launch_bounds__(kTmaThreads)
               p.out[gi] = o;
             } else if (MODE == kModeMVR) {
               if (wn) p.v_norm_out[gi] = cur;
-              const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
+              const double sval = FMA ? fma(-p.mu, cur, o) : __dsub_rn(o, __dmul_rn(p.mu, cur));
               if (inj) {
                 if (k % nu == 0) {
                   p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sval;
@@ -317,7 +321,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (p.x_out) p.x_out[gi] = cur;
               if (p.out) p.out[gi] = o;
-              if (p.partials) dot = __dadd_rn(dot, __dmul_rn(o, v0v[r]));
+              if (p.partials) dot = FMA ? fma(o, v0v[r], dot) : __dadd_rn(dot, __dmul_rn(o, v0v[r]));
             }
           }
           qprev[r] = Qu;
@@ -660,13 +664,13 @@ bool encode_1d(CUtensorMap *map, const double *base, int64_t n) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED>
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA = false>
 int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
             int *n_partials, double bytes, int cat) {
   constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
   constexpr int ROWS = (DIM == 2) ? R + 2 : R;
   const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
-  auto kern = (DIM == 2) ? march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED>
+  auto kern = (DIM == 2) ? march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED, FMA>
                          : march_tma_1d_kernel<MODE, R, S, VAR, GATHER, SCALED>;
   static int occ = -1;
   if (occ < 0) {
@@ -771,6 +775,11 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       break;
     case kModeMVR:
       if (d2) {
+        if (p.fma && !var && scaled && cfg_mvr == 0) {
+          rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
+                                                                     bytes, cat);
+          break;
+        }
         switch (cfg_mvr) {
           case 1: PMK_RUN(kModeMVR, 2, 4, 4, false); break;
           case 2: PMK_RUN(kModeMVR, 2, 8, 3, false); break;
@@ -787,6 +796,9 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       if (d2) {
         if (gather) {
           PMK_RUN(kModeIMV, 2, 4, 3, true);
+        } else if (p.fma && !var && !scaled && cfg_imv == 0) {
+          rc = run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s, n_partials,
+                                                                      bytes, cat);
         } else {
           switch (cfg_imv) {
             case 1: PMK_RUN(kModeIMV, 2, 4, 3, false); break;
