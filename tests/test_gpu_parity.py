@@ -121,6 +121,34 @@ def test_fgmres_internals_vs_oracle(name):
     assert rel(x.cpu().numpy(), xo) <= 1e-10
 
 
+@pytest.mark.parametrize("name", ["c3_small", "c5_small", "c2_small"])
+def test_orthogonality_and_arnoldi_relation(name):
+    """SURVEY section 4 known answers: the one-reduce orthogonalisation loses
+    orthogonality like the reference's MGS (c3_small: 9.6e-8 both after 12
+    iterations) and the Arnoldi relation A Z = V H holds to rounding."""
+    from oracle import pintmk_oracle as O
+    from paper_2401_00228_b200 import fgmres
+
+    case = SMALL[name]
+    h = gpu_hierarchy(case)
+    oh = oracle_hierarchy(case)
+    rhs = oh.rhs.ravel()
+    _, rep = fgmres(h, 0, rhs, tol=None, max_iter=12, keep_basis=True)
+    _, info = O.fgmres(oh, 0, rhs, None, 12, keep_basis=True)
+
+    def loss(basis):
+        V = np.stack(basis, axis=1)
+        return float(np.abs(V.T @ V - np.eye(V.shape[1])).max())
+
+    ours, ref = loss(rep.metadata["basis"]), loss(info["basis"])
+    assert ours <= 4.0 * ref + 1e-13, (ours, ref)
+    Z = np.stack(rep.metadata["preconditioned"], axis=1)
+    V = np.stack(rep.metadata["basis"][:Z.shape[1] + 1], axis=1)
+    AZ = np.stack([O.matvec(oh.fine, Z[:, j]) for j in range(Z.shape[1])], axis=1)
+    arn = np.linalg.norm(AZ - V @ rep.metadata["hessenberg"]) / np.linalg.norm(AZ)
+    assert arn <= 1e-14, arn
+
+
 _CLASSIC_SCRIPT = r"""
 import json, sys
 import numpy as np
