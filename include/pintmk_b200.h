@@ -228,6 +228,14 @@ int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *v_out,
                     double *w_next, double *child_out, pmk_stream_t stream);
 int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x,
                       pmk_stream_t stream);
+/* finish restricted to the time slices [row_begin, row_end) of x (row_begin a
+ * multiple of the level's coarsening factor nu); the call with row_begin = 0
+ * also runs the back substitution, so it must come first.  Lets the caller
+ * stream the finished part of x (e.g. to the host) while the rest is
+ * assembled.  Same result as pmk_fgmres_finish. */
+int pmk_fgmres_finish_rows(pmk_hier *H, int32_t idx, double *x,
+                           int32_t row_begin, int32_t row_end,
+                           pmk_stream_t stream);
 /* Copies the level's fgmres state to the host (synchronises the stream):
  * scalars[4] = {beta, rel, n_iter, breakdown}; hist[cap] (residual history),
  * hraw[(cap+1)*cap] (unrotated Hessenberg, row-major, ld = cap) and y[cap]

@@ -81,6 +81,8 @@ SIGNATURES = {
     "pmk_fgmres_step": (c_int32, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_void_p,
                                   c_void_p]),
     "pmk_fgmres_finish": (c_int32, [c_void_p, c_int32, c_void_p, c_void_p]),
+    "pmk_fgmres_finish_rows": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int32,
+                                         c_void_p]),
     "pmk_fgmres_state": (c_int32, [c_void_p, c_int32, POINTER(c_double), POINTER(c_double),
                                    POINTER(c_double), POINTER(c_double), POINTER(c_int32),
                                    c_void_p]),

@@ -242,7 +242,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
 int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double *v_scale,
            const double *vt, double *x, double *w, const double *v0, const double *v0_scale,
            double *partials, int *n_partials, const int *live, cudaStream_t s,
-           bool fused = false) {
+           bool fused = false, double *pj = nullptr, int *pj_done = nullptr) {
   MarchParams p = base_params(L);
   p.fma = fused ? 1 : 0;
   p.v = v;
@@ -256,6 +256,8 @@ int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double 
   p.v0 = v0;
   p.v0_scale = v0_scale;
   p.partials = partials;
+  p.pj = pj;
+  p.pj_done = pj_done;
   p.live = live;
   return launch_march(kModeIMV, p, s, n_partials);
 }
@@ -270,7 +272,7 @@ int alloc_state(LevelRT &R, int cap) {
   const size_t n_groups = (size_t)(cap + kDotGroup - 1) / kDotGroup;
   const size_t n_dotp = n_groups * (2 * kDotGroup + 1) * kMaxPartials;
   const size_t n_doubles =
-      2 * nh + (size_t)cap * cap + 7 * (size_t)(cap + 1) + 2 * kMaxPartials + n_dotp;
+      2 * nh + (size_t)cap * cap + 7 * (size_t)(cap + 1) + 4 * kMaxPartials + n_dotp;
   const size_t bytes = sizeof(KState) + 64 + n_doubles * sizeof(double);
   PMK_CUDA_TRY(cudaMalloc(&R.d_block, bytes));
   PMK_CUDA_TRY(cudaMemset(R.d_block, 0, bytes));
@@ -295,8 +297,8 @@ int alloc_state(LevelRT &R, int cap) {
   h.hist = d;
   d += cap + 1;
   d += cap + 1;  // spare
-  R.partA = d;
-  d += kMaxPartials;
+  R.partA = d;  // K-IMV <w, v_0>, then the pj block (<w, v_j>, <v_j, v_0>)
+  d += 3 * kMaxPartials;
   R.partB = d;
   d += kMaxPartials;
   h.gram = d;
@@ -428,7 +430,7 @@ int mvr_into_child(pmk_hier *H, int idx, const double *v, const double *v_scale,
 }
 
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
-                cudaStream_t s) {
+                cudaStream_t s, bool keep_w = true) {
   prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
@@ -457,16 +459,23 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     rc = child_solve(H, idx, child_out, live, s);
   }
   if (rc) return rc;
-  // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407)
-  int np = 0;
+  // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407);
+  // for j >= 1 also <w, v_j> and <v_j, v_0> off the staged v_j
+  int np = 0, pj_done = 0;
+  static const bool pj_on = [] {  // PMK_PJ=0: the dot pass takes v_0 and v_j too
+    const char *e = getenv("PMK_PJ");
+    return !(e && e[0] == '0');
+  }();
+  double *pj = (j >= 1 && !classic_mgs() && pj_on) ? R.partA + kMaxPartials : nullptr;
   rc = do_imv(R.L, R.P, v_out, nullptr, child_out, nullptr, w_next, R.v[0], nullptr, R.partA,
-              &np, live, s, !classic_mgs());
+              &np, live, s, !classic_mgs(), pj, &pj_done);
   if (rc) return rc;
   if (!classic_mgs()) {
-    // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412)
+    // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412);
+    // the last step of a fixed-budget inner solve needs only ||w||, not w
     int n_norm = 0;
-    rc = launch_icwy_mgs(R.d_state, R.cap, j, w_next, R.v.data(), R.N, R.partA, np, R.partM,
-                         R.partB, &n_norm, s);
+    rc = launch_icwy_mgs(R.d_state, R.cap, j, w_next, R.v.data(), R.N, R.partA, np,
+                         pj_done ? pj : nullptr, R.partM, R.partB, &n_norm, keep_w, s);
     if (rc) return rc;
     rc = launch_finish_col(R.d_state, R.cap, j, R.partB, n_norm, R.tol, s);
     if (rc) return rc;
@@ -494,34 +503,54 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   return 0;
 }
 
-int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
+// Back substitution (when row0 == 0) and x = sum_i y_i (v_i - Z vt_i) over
+// fine slices [row0, row1).  row0 is a multiple of nu: slice nu J closes
+// coarse slice J, so the sub-range starting there is itself a (shorter)
+// space-time vector whose slice 0 maps to coarse slice J, exactly the
+// assembly's slice mapping -- it runs on offset views.
+int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cudaStream_t s) {
   prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
   PMK_RETURN_IF(!x, PMK_ERR_ARG);
-  int rc = launch_backsolve(R.d_state, R.cap, s);
-  if (rc) return rc;
-  const int n = (int)R.vt.size();
   const int m = R.P.m_fine;
+  const int rows = (int)(R.N / m);
+  const int nu = R.P.mgrit ? 1 : R.P.nu;
+  PMK_RETURN_IF(row0 < 0 || row1 > rows || row0 >= row1 || row0 % nu != 0, PMK_ERR_ARG);
+  int rc = 0;
+  if (row0 == 0) {
+    rc = launch_backsolve(R.d_state, R.cap, s);
+    if (rc) return rc;
+  }
+  const int64_t off = (int64_t)row0 * m;
+  const int64_t coff = (int64_t)(row0 / nu) * (R.P.mgrit ? m : R.P.m_coarse);
+  const int64_t n_sub = (int64_t)(row1 - row0) * m;
+  const int n = (int)R.vt.size();
   int first = 0;
   do {
     AssembleArgs a;
     std::memset(&a, 0, sizeof(a));
     a.count = 0;
     for (int l = first; l < n && a.count < kAsmChunk; ++l) {
-      a.v[a.count] = R.v[l];
-      a.vt[a.count] = R.vt[l];
+      a.v[a.count] = R.v[l] + off;
+      a.vt[a.count] = R.vt[l] + coff;
       ++a.count;
     }
     if (R.P.mgrit)  // vt_l are the interpolated fine vectors
-      rc = launch_assemble(R.d_state, a, x, R.N, m, 1, m, nullptr, first, s);
+      rc = launch_assemble(R.d_state, a, x + off, n_sub, m, 1, m, nullptr, first, s);
     else
-      rc = launch_assemble(R.d_state, a, x, R.N, m, R.P.nu, R.P.m_coarse, R.P.group_of, first,
-                           s);
+      rc = launch_assemble(R.d_state, a, x + off, n_sub, m, R.P.nu, R.P.m_coarse,
+                           R.P.group_of, first, s);
     if (rc) return rc;
     first += kAsmChunk;
   } while (first < n);
   return 0;
+}
+
+int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
+  return fgmres_finish_rows(H, idx, x, 0, (int)(R.N / R.P.m_fine), s);
 }
 
 int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s) {
@@ -533,7 +562,7 @@ int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaSt
   int rc = fgmres_begin(H, idx, R.rhs, R.budget, 0.0, parent_live, s);
   if (rc) return rc;
   for (int j = 0; j < R.budget; ++j) {
-    rc = fgmres_step(H, idx, j, R.v_slots[j], R.w_buf, R.child_out[j], s);
+    rc = fgmres_step(H, idx, j, R.v_slots[j], R.w_buf, R.child_out[j], s, j + 1 < R.budget);
     if (rc) return rc;
   }
   return fgmres_finish(H, idx, x, s);
@@ -807,6 +836,12 @@ int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *v_out, double *
 int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x, pmk_stream_t stream) {
   PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
   return fgmres_finish(H, idx, x, cs(stream));
+}
+
+int pmk_fgmres_finish_rows(pmk_hier *H, int32_t idx, double *x, int32_t row_begin,
+                           int32_t row_end, pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1, PMK_ERR_ARG);
+  return fgmres_finish_rows(H, idx, x, row_begin, row_end, cs(stream));
 }
 
 int pmk_fgmres_state(pmk_hier *H, int32_t idx, double *scalars, double *hist, double *hraw,

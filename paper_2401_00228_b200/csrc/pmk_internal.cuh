@@ -176,6 +176,12 @@ struct MarchParams {
   const double *v0;
   const double *v0_scale;
   double *partials;  // one per block (dot(w, v0))
+  // optional (IMV, v != v0): partial <w, v> at pj[b] and <v, v0> at
+  // pj[kMaxPartials + b], b < *n_partials, read off the staged input v (the
+  // ICWY dot pass then skips v_0 and v_j).  Produced by the 2-D TMA path
+  // only; the launcher reports whether it did in *pj_done (host pointer).
+  double *pj;
+  int *pj_done;
   const int *live;
 };
 

@@ -362,28 +362,37 @@ __device__ __forceinline__ double warp_reduce_partials(const double *p, int n) {
 // Reduce the dot partials, store Gram row j, solve (I + L) h = c and write
 // column j of H (rows 0..j).  One block.
 //   c_0 = <w, v_0>: K-IMV partials (c0p, n_c0); for j >= 1 the group passes
-//   wrote, per group g (basis 0..j-1 in groups of kGroup, slots as above),
+//   wrote, per group g (basis o..j-1 in groups of kDotGroup, slots as above),
 //   <w, v_i> for i >= 1, <v_j, v_i>, and <w, v_j> (taken from group 0).
+//   With pj (o = 1), K-IMV also produced <w, v_j> (pj) and <v_j, v_0>
+//   (pj + kMaxPartials) and the group passes start at v_1.
 __global__ void __launch_bounds__(1024)
     icwy_solve_kernel(KState *st, int ld, int j, const double *c0p, int n_c0,
-                      const double *gp, int n_gp) {
+                      const double *pj, const double *gp, int n_gp) {
   if (!st->live) return;
   extern __shared__ double sh[];  // c[0..j], g[0..j-1]
   double *c = sh, *g = sh + (j + 1);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int gstride = (2 * kDotGroup + 1) * n_gp;  // doubles per group
+  const int o = pj ? 1 : 0;                         // first basis vector of group 0
   for (int d = warp; d < 2 * j + 1; d += nw) {
     double x;
     if (d == 0) {
       x = warp_reduce_partials(c0p, n_c0);
     } else if (d < j) {  // <w, v_d>, 1 <= d < j
-      x = warp_reduce_partials(gp + (int64_t)(d / kDotGroup) * gstride + (d % kDotGroup) * n_gp, n_gp);
+      const int e = d - o;
+      x = warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride + (e % kDotGroup) * n_gp, n_gp);
     } else if (d == j) {  // <w, v_j>
-      x = warp_reduce_partials(gp + (int64_t)2 * kDotGroup * n_gp, n_gp);
+      x = pj ? warp_reduce_partials(pj, n_c0)
+             : warp_reduce_partials(gp + (int64_t)2 * kDotGroup * n_gp, n_gp);
     } else {  // <v_j, v_i>, i = d - j - 1
       const int i = d - j - 1;
-      x = warp_reduce_partials(
-          gp + (int64_t)(i / kDotGroup) * gstride + (kDotGroup + i % kDotGroup) * n_gp, n_gp);
+      const int e = i - o;
+      x = (pj && i == 0)
+              ? warp_reduce_partials(pj + kMaxPartials, n_c0)
+              : warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride +
+                                         (kDotGroup + e % kDotGroup) * n_gp,
+                                     n_gp);
     }
     if (lane == 0) {
       if (d <= j)
@@ -419,7 +428,7 @@ __global__ void __launch_bounds__(1024)
 template <int CNT>
 __global__ void __launch_bounds__(kRedThreads)
     icwy_update_vec_kernel(const KState *st, int ld, int j, int i0, MultiVec V,
-                           double *__restrict__ w, int64_t n, double *partials) {
+                           double *__restrict__ w, int64_t n, double *partials, bool store) {
   if (!st->live) return;
   constexpr int U = (12 / (CNT + 1)) > 1 ? 12 / (CNT + 1) : 1;
   double hq[CNT];
@@ -450,7 +459,7 @@ __global__ void __launch_bounds__(kRedThreads)
         a[u].x = __dsub_rn(a[u].x, __dmul_rn(hq[q], c[u][q].x));
         a[u].y = __dsub_rn(a[u].y, __dmul_rn(hq[q], c[u][q].y));
       }
-      w2[i + u * stride] = a[u];
+      if (store) w2[i + u * stride] = a[u];
       if (partials) acc[0] = dot2(acc[0], a[u], a[u]);
     }
   }
@@ -462,14 +471,14 @@ __global__ void __launch_bounds__(kRedThreads)
       a.x = __dsub_rn(a.x, __dmul_rn(hq[q], c.x));
       a.y = __dsub_rn(a.y, __dmul_rn(hq[q], c.y));
     }
-    w2[i] = a;
+    if (store) w2[i] = a;
     if (partials) acc[0] = dot2(acc[0], a, a);
   }
   if ((n & 1) && t0 == stride - 1) {
     double a = w[n - 1];
 #pragma unroll
     for (int q = 0; q < CNT; ++q) a = __dsub_rn(a, __dmul_rn(hq[q], V.v[q][n - 1]));
-    w[n - 1] = a;
+    if (store) w[n - 1] = a;
     if (partials) acc[0] = __dadd_rn(acc[0], __dmul_rn(a, a));
   }
   if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(kRedThreads)
 
 __global__ void __launch_bounds__(kRedThreads)
     icwy_update_kernel(const KState *st, int ld, int j, int i0, MultiVec V, int count,
-                       double *__restrict__ w, int64_t n, double *partials) {
+                       double *__restrict__ w, int64_t n, double *partials, bool store) {
   if (!st->live) return;
   double hq[kGroup];
 #pragma unroll
@@ -489,7 +498,7 @@ __global__ void __launch_bounds__(kRedThreads)
 #pragma unroll
     for (int q = 0; q < kGroup; ++q)
       if (q < count) a = __dsub_rn(a, __dmul_rn(hq[q], V.v[q][i]));
-    w[i] = a;
+    if (store) w[i] = a;
     if (partials) acc[0] = __dadd_rn(acc[0], __dmul_rn(a, a));
   }
   if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
@@ -598,11 +607,11 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int q = 0; q < CNT; ++q) y[q] = (first + q < hi) ? st->y[first + q] : 0.0;
   const int chunk = 256 * U;
-  const int n_coarse = (rows - 1) / 2 + 1;
+  const int n_coarse = rows / 2 + 1;  // K = 0 and the pairs (2K-1, 2K)
   for (int K = blockIdx.y; K < n_coarse; K += gridDim.y) {
     const int64_t cbase = (int64_t)K * m;
     const int k0 = (K == 0) ? 0 : 2 * K - 1;
-    const bool two = K > 0;
+    const bool two = K > 0 && k0 + 1 < rows;  // (a row-range view may end on 2K-1)
     for (int i0 = blockIdx.x * chunk; i0 < m; i0 += gridDim.x * chunk) {
       double tt[U][CNT], v0[U][CNT], v1[U][CNT], a0[U], a1[U];
 #pragma unroll
@@ -766,9 +775,9 @@ void dots_vec(const KState *st, const double *w, const double *vj, const MultiVe
 }
 template <int CNT>
 void update_vec(const KState *st, int ld, int j, int i0, const MultiVec &V, double *w, int64_t n,
-                double *partials, cudaStream_t s) {
+                double *partials, bool store, cudaStream_t s) {
   icwy_update_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, w, n,
-                                                                 partials);
+                                                                 partials, store);
 }
 
 #define PMK_CASES8(F) F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8)
@@ -778,13 +787,16 @@ void update_vec(const KState *st, int ld, int j, int i0, const MultiVec &V, doub
 // leave the partials of ||w||^2 in `norm_partials` (*n_norm of them).  All
 // passes use the fixed kRedBlocks grid (deterministic partial layout).
 int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
-                    const double *c0p, int n_c0, double *dot_partials, double *norm_partials,
-                    int *n_norm, cudaStream_t s) {
+                    const double *c0p, int n_c0, const double *pj, double *dot_partials,
+                    double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s) {
   auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   bool vec = al(w);
   for (int i = 0; i <= j; ++i) vec = vec && al(v[i]);
   const int64_t gstride = (int64_t)(2 * kDotGroup + 1) * kRedBlocks;
-  for (int i0 = 0, gi = 0; i0 < j; i0 += kDotGroup, ++gi) {
+  if (j < 1) pj = nullptr;
+  // with pj the K-IMV pass already produced every dot involving v_0 or v_j
+  // except the Gram entries <v_j, v_i>, 0 < i < j
+  for (int i0 = pj ? 1 : 0, gi = 0; i0 < j; i0 += kDotGroup, ++gi) {
     const int cnt = (j - i0 < kDotGroup) ? j - i0 : kDotGroup;
     MultiVec V{};
     for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
@@ -809,7 +821,7 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
   }
   {
     prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
-    icwy_solve_kernel<<<1, 1024, (2 * j + 1) * sizeof(double), s>>>(st, ld, j, c0p, n_c0,
+    icwy_solve_kernel<<<1, 1024, (2 * j + 1) * sizeof(double), s>>>(st, ld, j, c0p, n_c0, pj,
                                                                    dot_partials, kRedBlocks);
     PMK_LAUNCH_CHECK();
   }
@@ -818,14 +830,15 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
     const bool last = i0 + cnt > j;
     MultiVec V{};
     for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
-    prof::Scope scope(prof::kMGS, 8.0 * (cnt + 2) * (double)n,
+    const bool store = keep_w || !last;
+    prof::Scope scope(prof::kMGS, 8.0 * (cnt + (store ? 2 : 1)) * (double)n,
                       2.0 * (cnt + (last ? 1 : 0)) * (double)n, s);
     double *part = last ? norm_partials : nullptr;
     if (vec) {
       switch (cnt) {
 #define PMK_UPD_CASE(C)                                \
   case C:                                              \
-    update_vec<C>(st, ld, j, i0, V, w, n, part, s);    \
+    update_vec<C>(st, ld, j, i0, V, w, n, part, store, s); \
     break;
         PMK_CASES16(PMK_UPD_CASE)
 #undef PMK_UPD_CASE
@@ -833,7 +846,8 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
           return PMK_ERR_ARG;
       }
     } else {
-      icwy_update_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, cnt, w, n, part);
+      icwy_update_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, cnt, w, n, part,
+                                                            store);
     }
     PMK_LAUNCH_CHECK();
   }
@@ -867,7 +881,7 @@ int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t 
     const int u = (12 / (3 * a.count)) > 1 ? 12 / (3 * a.count) : 1;
     const int xb = (m + 256 * u - 1) / (256 * u);
     const int target = 8 * kSMs * 8;  // ~8 waves of 8 resident blocks per SM
-    const int n_coarse = (rows - 1) / 2 + 1;
+    const int n_coarse = rows / 2 + 1;  // K = 0 and the pairs (2K-1, 2K)
     int yb = (target + xb - 1) / xb;
     if (yb > n_coarse) yb = n_coarse;
     dim3 grid(xb, yb < 1 ? 1 : yb);

@@ -38,8 +38,8 @@ struct MultiVec {
 };
 // dot partial buffer: ceil(cap / kDotGroup) * (2 kDotGroup + 1) * kMaxPartials doubles
 int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
-                    const double *c0p, int n_c0, double *dot_partials, double *norm_partials,
-                    int *n_norm, cudaStream_t s);
+                    const double *c0p, int n_c0, const double *pj, double *dot_partials,
+                    double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s);
 
 int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
                  cudaStream_t s);

@@ -279,6 +279,7 @@ double march_bytes(int mode, const MarchParams &p, int *cat) {
 
 int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials) {
   if (mode != kModeMV && mode != kModeMVR && mode != kModeIMV) return PMK_ERR_ARG;
+  if (p.pj_done) *p.pj_done = 0;
   int cat = 0;
   const double bytes = march_bytes(mode, p, &cat);
   static const bool force_reg = getenv("PMK_MARCH_REG") != nullptr;

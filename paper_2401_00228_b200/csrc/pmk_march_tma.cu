@@ -133,6 +133,10 @@ __global__ void __launch_bounds__(kTmaThreads)
   // (within 1 ulp of the division; exact_scale launches take the register path)
   const double vrcp = SCALED ? __drcp_rn(*p.v_scale) : 1.0;
   double dot = 0.0;
+  double dwj = 0.0, dgj = 0.0;  // K-IMV with pj: <w, v>, <v, v0>
+  // (in-solver variant only; run_tma reports it through p.pj_done)
+  constexpr bool kPj = MODE == kModeIMV && DIM == 2 && FMA && !VAR && !GATHER;
+  const bool wantj = kPj && p.pj != nullptr;
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -180,9 +184,12 @@ __global__ void __launch_bounds__(kTmaThreads)
     const int x = g.single ? t : x0 + t;
     const bool xin = (g.single ? t < nx : t < g.tile_w) && x < nx;
     const bool hw = x > 0, he = x < nx - 1;
-    // this thread's pre-pass grid column (box element t + row shift)
-    const int px = boxx + t;
-    const bool pin = t < kBox - 1 && px >= 0 && px < nx;
+    // this thread's pre-pass box element: the one holding its own output
+    // column (box element x - boxx, so that the staged input of its outputs
+    // stays in registers); on split rows thread kBox-1 takes element 0.
+    const int pe = g.single ? t : ((t == kBox - 1) ? 0 : t + 1);
+    const int px = boxx + pe;
+    const bool pin = pe < kBox - 1 && px >= 0 && px < nx;
 
     double qprev[RO], acc[RO];
 #pragma unroll
@@ -213,20 +220,35 @@ __global__ void __launch_bounds__(kTmaThreads)
                         ? __ldg(p.v0 + (int64_t)kf * m + gx0 + r * nx)
                         : 0.0;
     }
+    int Kc = (kstart == 0) ? 0 : (kstart - 1) / nu + 1;
+    int posc = (kstart == 0) ? nu - 1 : (kstart - 1) - (Kc - 1) * nu;
+    int dnext = (p.dropped && kstart < ke) ? p.dropped[kstart] : 0;
     for (int i = 0; i < nsl; ++i, ++it) {
       // ---- per-slice uniform quantities
       const int k = kstart + i;
       const bool prime = k < kb;
       const int stage = (int)(it % S);
       double *sv = smem + (size_t)stage * NB * ROWS * kBox;
-      const int K = (k == 0) ? 0 : (k - 1) / nu + 1;  // coarse slice of k
-      const int pos = (k == 0) ? nu - 1 : (k - 1) - (K - 1) * nu;
-      const bool drop = p.dropped && p.dropped[k];
+      // coarse slice K of k and position in its slab (stepped, no division)
+      const int K = Kc, pos = posc;
+      if (k == 0) {
+        Kc = 1;
+        posc = 0;
+      } else if (++posc == nu) {
+        ++Kc;
+        posc = 0;
+      }
+      // dropped coupling of k: loaded one slice ahead, off the critical path
+      const bool drop = dnext != 0;
+      if (p.dropped && k + 1 < ke) dnext = p.dropped[k + 1];
       const int pk = (int)(((int64_t)k * m + boxx) & 1);  // row parity shifts (issue())
       const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
       const int64_t kofs = (int64_t)k * m;
       // IMV: v_0 of this slice (prefetched one slice ahead) for the dot
       double v0v[RO];
+      double vj[RO];  // the staged input at this thread's outputs (pj dots)
+#pragma unroll
+      for (int r = 0; r < RO; ++r) vj[r] = 0.0;
       if (MODE == kModeIMV && p.partials) {
 #pragma unroll
         for (int r = 0; r < RO; ++r) v0v[r] = v0next[r];
@@ -245,14 +267,13 @@ __global__ void __launch_bounds__(kTmaThreads)
         for (int r = 0; r < ROWS; ++r) {
           if (r < rlo || r > rhi) continue;
           const int y = (DIM == 2) ? y0 - 1 + r : 0;
-          double *cell = sv + r * kBox + t + ((pk + (y & nx)) & 1);
+          double *cell = sv + r * kBox + pe + ((pk + (y & nx)) & 1);
           double u = *cell;
-          // 0 / scale = 0 (scale > 0): skipping it keeps exact zeros (the
-          // first Krylov vector is mostly zero) off the division slow path
           if (SCALED) u = __dmul_rn(u, vrcp);
           if (MODE == kModeIMV) {
+            if (kPj && r >= 1 && r <= R) vj[r - 1] = u;
             const double z = GATHER ? __ldg(vtk + p.group_of[y * nx + px])
-                                    : sv[(ROWS + r) * kBox + t + ((pK + (y & nx)) & 1)];
+                                    : sv[(ROWS + r) * kBox + pe + ((pK + (y & nx)) & 1)];
             u = __dsub_rn(u, z);
           }
           *cell = u;
@@ -322,6 +343,10 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (p.x_out) p.x_out[gi] = cur;
               if (p.out) p.out[gi] = o;
               if (p.partials) dot = FMA ? fma(o, v0v[r], dot) : __dadd_rn(dot, __dmul_rn(o, v0v[r]));
+              if (wantj) {
+                dwj = fma(o, vj[r], dwj);
+                dgj = fma(vj[r], v0v[r], dgj);
+              }
             }
           }
           qprev[r] = Qu;
@@ -396,6 +421,10 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (p.partials) {
                 dot = __dadd_rn(dot, __dmul_rn(o, v0v[r]));
               }
+              if (wantj) {
+                dwj = fma(o, vj[r], dwj);
+                dgj = fma(vj[r], v0v[r], dgj);
+              }
             }
           }
           qprev[r] = Qu;
@@ -413,6 +442,14 @@ __global__ void __launch_bounds__(kTmaThreads)
   if (MODE == kModeIMV && p.partials) {
     const double s = block_sum(dot);
     if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
+  }
+  if (wantj) {
+    const double a = block_sum(dwj);
+    const double b = block_sum(dgj);
+    if (threadIdx.x == 0) {
+      p.pj[blockIdx.x] = a;
+      p.pj[kMaxPartials + blockIdx.x] = b;
+    }
   }
   if (MODE == kModeMVR && p.vh_partials) {
     const double s = block_sum(vsq);
@@ -519,14 +556,26 @@ __global__ void __launch_bounds__(kTmaThreads)
       for (int u = 0; u < SL; ++u)
         v0next[u] = (ok[u] && kf < ke) ? __ldg(p.v0 + (int64_t)kf * m + xs[u]) : 0.0;
     }
+    int Kc = (kstart == 0) ? 0 : (kstart - 1) / nu + 1;
+    int posc = (kstart == 0) ? nu - 1 : (kstart - 1) - (Kc - 1) * nu;
+    int dnext = (p.dropped && kstart < ke) ? p.dropped[kstart] : 0;
     for (int i = 0; i < nsl; ++i, ++it) {
       const int k = kstart + i;
       const bool prime = k < kb;
       const int stage = (int)(it % S);
       double *sv = smem + (size_t)stage * NB * R * kBox;
-      const int K = (k == 0) ? 0 : (k - 1) / nu + 1;
-      const int pos = (k == 0) ? nu - 1 : (k - 1) - (K - 1) * nu;
-      const bool drop = p.dropped && p.dropped[k];
+      // coarse slice K of k and position in its slab (stepped, no division)
+      const int K = Kc, pos = posc;
+      if (k == 0) {
+        Kc = 1;
+        posc = 0;
+      } else if (++posc == nu) {
+        ++Kc;
+        posc = 0;
+      }
+      // dropped coupling of k: loaded one slice ahead, off the critical path
+      const bool drop = dnext != 0;
+      if (p.dropped && k + 1 < ke) dnext = p.dropped[k + 1];
       const int pk = (int)(((int64_t)k * m + boxx) & 1);  // parity of box 0
       const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
       const int64_t kofs = (int64_t)k * m;
@@ -697,7 +746,12 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
   if (MODE != kModeMV && grid_cap > kMaxPartials) grid_cap = kMaxPartials;  // partials
   // ~8 work items per resident CTA; chunks of at most 32 units (one extra
   // prime slice per chunk, served from L2).
-  int64_t upc = ((int64_t)n_units * tiles) / (8LL * grid_cap);
+  static const int ipc = [] {  // work items per resident CTA (tuning knob PMK_IPC)
+    const char *e = getenv("PMK_IPC");
+    const int v = e ? atoi(e) : 8;
+    return v > 0 ? v : 8;
+  }();
+  int64_t upc = ((int64_t)n_units * tiles) / ((int64_t)ipc * grid_cap);
   if (upc < 2) upc = 2;
   if (upc > 32) upc = 32;
   g.upc = (int)upc;
@@ -713,6 +767,8 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
   prof::Scope scope(cat, bytes, 0.0, s);
   kern<<<grid, kTmaThreads, smem, s>>>(p, mv, mvt, g);
   PMK_LAUNCH_CHECK();
+  if (MODE == kModeIMV && DIM == 2 && FMA && !VAR && !GATHER && p.pj && p.pj_done)
+    *p.pj_done = 1;
   if (n_partials) *n_partials = grid;
   return 0;
 }

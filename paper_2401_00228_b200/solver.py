@@ -464,7 +464,7 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
 
 
 def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_iter: int,
-            keep_basis: bool = False):
+            keep_basis: bool = False, copier=None):
     import torch
 
     if not 0 <= level_idx < hier.n_levels - 1:
@@ -503,7 +503,14 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
             if st["breakdown"] or st["rel"] <= tol:
                 break
     x = _empty(lvl.total_dim)
-    _lib.check(lib.pmk_fgmres_finish(H, level_idx, _lib.ptr(x), s), "fgmres_finish")
+    if copier is None:
+        _lib.check(lib.pmk_fgmres_finish(H, level_idx, _lib.ptr(x), s), "fgmres_finish")
+    else:  # assemble x in slabs of time slices, each copied out while the next is built
+        for r0, r1 in _slabs(lvl.n_steps + 1, _nu_of(lvl), _RESULT_SLABS):
+            _lib.check(lib.pmk_fgmres_finish_rows(H, level_idx, _lib.ptr(x), r0, r1, s),
+                       "fgmres_finish_rows")
+            copier.start(x, r0 * lvl.state_dim, r1 * lvl.state_dim)
+        copier.src = x
     st = _state(hier, level_idx, want_arrays=True)
     n_iter = st["n_iter"]
     report.outer_iterations = n_iter
@@ -524,7 +531,73 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
     return x, report
 
 
-def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart: int):
+_RESULT_SLABS = 8
+
+
+def _nu_of(lvl) -> int:
+    pair = lvl.pair
+    return 1 if isinstance(pair, MgritPair) else int(getattr(pair, "nu", 1))
+
+
+def _slabs(rows: int, nu: int, n: int):
+    """[r0, r1) ranges covering rows, every r0 a multiple of nu."""
+    step = max(nu, ((rows + n - 1) // n + nu - 1) // nu * nu)
+    return [(r0, min(rows, r0 + step)) for r0 in range(0, rows, step)]
+
+
+class _ResultCopy:
+    """Device -> host copy of the solution on a side stream, started as soon
+    as a candidate x exists, so that it overlaps the true-residual check
+    (stepper.py:191-193) that follows; a further restart cycle first waits
+    for the copy to finish reading x."""
+
+    def __init__(self, out):
+        import torch
+
+        self.out = out
+        self.stream = _copy_stream(torch.cuda.current_device())
+        self.src = None
+
+    def start(self, x, lo: int = 0, hi: int | None = None):
+        """Copy x[lo:hi] (all of x by default) once the current stream has
+        produced it."""
+        import torch
+
+        self.stream.wait_stream(torch.cuda.current_stream())
+        xf, of = x.reshape(-1), self.out.reshape(-1)
+        hi = xf.numel() if hi is None else hi
+        with torch.cuda.stream(self.stream):
+            of[lo:hi].copy_(xf[lo:hi], non_blocking=True)
+        self.src = x
+
+    def fence(self):
+        """x is about to change on the current stream."""
+        import torch
+
+        if self.src is not None:
+            torch.cuda.current_stream().wait_stream(self.stream)
+            self.src = None
+
+    def done(self, x) -> bool:
+        """Wait for the copy; True when it holds x."""
+        self.stream.synchronize()
+        return self.src is x
+
+
+_COPY_STREAMS: dict = {}
+
+
+def _copy_stream(device: int):
+    import torch
+
+    st = _COPY_STREAMS.get(device)
+    if st is None:
+        st = _COPY_STREAMS[device] = torch.cuda.Stream(device=device)
+    return st
+
+
+def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart: int,
+                      copier: _ResultCopy | None = None):
     """FGMRES(m): cycles of the reference fgmres on the current residual
     (SURVEY.md section 8(c) restart oracle)."""
     import torch
@@ -546,11 +619,17 @@ def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart:
             final_rel = 0.0
             break
         m = min(restart, max_outer - total)
-        dx, rep = _fgmres(hier, 0, r, tol=tol * beta0 / rn, max_iter=m)
-        if x is None:
-            x = dx
+        first = x is None
+        dx, rep = _fgmres(hier, 0, r, tol=tol * beta0 / rn, max_iter=m,
+                          copier=copier if first else None)
+        if first:
+            x = dx  # (copied out slab by slab as it was assembled)
         else:
+            if copier is not None:
+                copier.fence()
             x.add_(dx)
+            if copier is not None:
+                copier.start(x)
         del dx
         total += rep.outer_iterations
         cycles += 1
@@ -595,14 +674,25 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     torch.cuda.synchronize()
     if ledger is not None:  # real-time phase ledger (ledger.py): every launch timed
         _lib.profile_begin(True)
+    if output is None:
+        output = "host" if hier.fine.host_io else "device"
+    if out is None and output == "host":
+        # pinned (torch's caching host allocator): a fast D2H that can overlap
+        out = torch.empty(hier.fine.rhs.numel(), dtype=torch.float64, pin_memory=True)
+        host_out = True
+    else:
+        host_out = False
+    copier = _ResultCopy(out) if out is not None and out.device.type == "cpu" else None
     t0 = time.perf_counter()
     try:
         with hier.on_stream():
             if cfg.restart is None:
-                x, report = _fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer)
+                x, report = _fgmres(hier, 0, rhs, tol=cfg.tol, max_iter=cfg.max_outer,
+                                    copier=copier)
             else:
-                x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart)
-        torch.cuda.synchronize()
+                x, report = _restarted_fgmres(hier, cfg.tol, cfg.max_outer, cfg.restart,
+                                              copier)
+        torch.cuda.current_stream().synchronize()  # (not the result copy's stream)
         report.method = method_name
         report.wall_time = time.perf_counter() - t0
         report.tol = cfg.tol
@@ -625,12 +715,11 @@ def _solve(hier: LevelHierarchy, ledger, model, method_name: str, output: str | 
     report.converged = true_res <= cfg.tol
     report.level_stats = {"levels": hier.describe(), "moves": hier.moves}
     if out is not None:
-        out.copy_(x.reshape(out.shape))  # e.g. into a pinned host buffer
+        if copier is None or not copier.done(x):
+            out.copy_(x.reshape(out.shape))  # e.g. into a pinned host buffer
+        if host_out:
+            return out.numpy(), report
         return out, report
-    if output is None:
-        output = "host" if hier.fine.host_io else "device"
-    if output == "host":
-        return x.cpu().numpy(), report
     return x, report
 
 

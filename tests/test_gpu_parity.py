@@ -216,6 +216,31 @@ def test_device_io_roundtrip():
     np.testing.assert_array_equal(xd.cpu().numpy(), xh)
 
 
+@pytest.mark.parametrize("name", ["c1_small", "c2_small", "c4_small", "c5_small",
+                                  "ts2_small", "mgrit1_small", "mgrit2_dec_small"])
+def test_host_output_slabs_bitwise(name):
+    """x assembled slab by slab (pmk_fgmres_finish_rows) and streamed into a
+    host buffer equals the one-launch device assembly bitwise: time pairs
+    (nu = 2, 4), agglomerated TS pairs, MGRIT, with and without restarts."""
+    import torch
+
+    from paper_2401_00228_b200 import multilevel_solve
+
+    case = SMALL[name]
+    for restart in (None, 5):
+        c = case.scaled(restart=restart) if restart else case
+        u0 = torch.from_numpy(c.u0_vector())
+        xd, rd = multilevel_solve(gpu_hierarchy(c, u0=u0.cuda()))
+        pin = torch.full((c.N,), float("nan"), dtype=torch.float64).pin_memory()
+        xo, ro = multilevel_solve(gpu_hierarchy(c, u0=u0.cuda()), out=pin)
+        assert xo is pin
+        np.testing.assert_array_equal(pin.numpy(), xd.cpu().numpy())
+        xn, _ = multilevel_solve(gpu_hierarchy(c))  # numpy in -> numpy out
+        assert isinstance(xn, np.ndarray)
+        np.testing.assert_array_equal(xn, xd.cpu().numpy())
+        assert ro.outer_iterations == rd.outer_iterations
+
+
 def test_sequential_solve_matches_oracle():
     from oracle import pintmk_oracle as O
     from paper_2401_00228_b200 import (ThetaSchemeConfig, build_laplacian,
