@@ -15,6 +15,9 @@ def short_name(name: str) -> str:
     m = re.search(r"march_tma_kernel<(?:\(int\))?(\d), (?:\(int\))?(\d)", name)
     if m:
         return {"0": "march_mv", "1": "march_mvr", "2": "march_imv"}[m.group(1)] + f"[{m.group(2)}d]"
+    m = re.search(r"march_lean_kernel<(?:\(int\))?(\d)", name)
+    if m:
+        return {"1": "march_mvr", "2": "march_imv"}[m.group(1)] + "[2d]"
     m = re.search(r"march_tma_1d_kernel<(?:\(int\))?(\d)", name)
     if m:
         return {"0": "march_mv", "1": "march_mvr", "2": "march_imv"}[m.group(1)] + "[1d]"

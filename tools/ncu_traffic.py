@@ -12,8 +12,8 @@ import re
 import sys
 
 CATS = [(r"march_tma(?:_1d)?_kernel<(?:\(int\))?0", "march_mv"),
-        (r"march_tma(?:_1d)?_kernel<(?:\(int\))?1", "march_mvr"),
-        (r"march_tma(?:_1d)?_kernel<(?:\(int\))?2", "march_imv"),
+        (r"march_(?:tma(?:_1d)?|lean)_kernel<(?:\(int\))?1", "march_mvr"),
+        (r"march_(?:tma(?:_1d)?|lean)_kernel<(?:\(int\))?2", "march_imv"),
         (r"mgs_pass|icwy_dots|icwy_update", "mgs_pass"),
         (r"dot_partials|diffsq_partials", "reduce"), (r"assemble", "assemble"),
         (r"dst_rows|dst_cols|dgemm", "coarse_gemm"),
