@@ -137,6 +137,15 @@ __global__ void __launch_bounds__(kTmaThreads)
   // (in-solver variant only; run_tma reports it through p.pj_done)
   constexpr bool kPj = MODE == kModeIMV && DIM == 2 && FMA && !VAR && !GATHER;
   const bool wantj = kPj && p.pj != nullptr;
+  // In-solver (FMA) launches honour a fixed contract, checked by the
+  // launcher: K-IMV writes w (p.out) and the <w, v_0> partials and no x;
+  // K-MVR writes the normalised v (p.v_norm_out).  Compile-time flags keep
+  // the per-row null tests (and their constant-bank reloads) out of the loop.
+  constexpr bool kSolver = FMA;
+  const bool has_out = kSolver ? (MODE != kModeMVR) : (p.out != nullptr);
+  const bool has_x = kSolver ? false : (p.x_out != nullptr);
+  const bool has_part = kSolver ? (MODE == kModeIMV) : (p.partials != nullptr);
+  const bool has_vn = kSolver ? (MODE == kModeMVR) : (p.v_norm_out != nullptr);
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -212,7 +221,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     const bool tile_interior = DIM == 2 && (R % 2 == 0) && rlo == 0 && y0 + R <= ny - 1;
     const bool warp_fast = __all_sync(0xffffffffu, tile_interior && xin && hw && he);
     double v0next[RO];
-    if (MODE == kModeIMV && p.partials) {
+    if (MODE == kModeIMV && has_part) {
       const int kf = (kb > kstart) ? kb : kstart;  // first non-prime slice
 #pragma unroll
       for (int r = 0; r < RO; ++r)
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       double vj[RO];  // the staged input at this thread's outputs (pj dots)
 #pragma unroll
       for (int r = 0; r < RO; ++r) vj[r] = 0.0;
-      if (MODE == kModeIMV && p.partials) {
+      if (MODE == kModeIMV && has_part) {
 #pragma unroll
         for (int r = 0; r < RO; ++r) v0v[r] = v0next[r];
         const int kn = k + 1;  // prefetch the next slice of this item
@@ -289,8 +298,11 @@ __global__ void __launch_bounds__(kTmaThreads)
         const double *col = sv + xo;
         double up = col[sh0];
         double cur = col[kBox + sh1];
-        const bool wn = MODE == kModeMVR && p.v_norm_out != nullptr;
+        const bool wn = MODE == kModeMVR && has_vn;
         const bool inj = MODE == kModeMVR && p.inject;
+        // slice-k base pointers at (y0, x); rows at + r nx
+        double *ob = (MODE == kModeMVR ? p.v_norm_out : p.out) + kofs + gx0;
+        double *hb = (MODE == kModeMVR) ? p.vh + (int64_t)K * m + gx0 : nullptr;
         const bool closes = pos == nu - 1, opens = pos == 0;
 #pragma unroll
         for (int r = 0; r < RO; ++r) {
@@ -325,7 +337,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             if (MODE == kModeMV) {
               p.out[gi] = o;
             } else if (MODE == kModeMVR) {
-              if (wn) p.v_norm_out[gi] = cur;
+              if (wn) ob[r * nx] = cur;
               const double sval = FMA ? fma(-p.mu, cur, o) : __dsub_rn(o, __dmul_rn(p.mu, cur));
               if (inj) {
                 if (k % nu == 0) {
@@ -335,14 +347,14 @@ __global__ void __launch_bounds__(kTmaThreads)
               } else {
                 acc[r] = opens ? sval : __dadd_rn(acc[r], sval);
                 if (closes) {
-                  p.vh[(int64_t)K * m + gx0 + r * nx] = acc[r];
+                  hb[r * nx] = acc[r];
                   vsq = __dadd_rn(vsq, __dmul_rn(acc[r], acc[r]));
                 }
               }
             } else {
-              if (p.x_out) p.x_out[gi] = cur;
-              if (p.out) p.out[gi] = o;
-              if (p.partials) dot = FMA ? fma(o, v0v[r], dot) : __dadd_rn(dot, __dmul_rn(o, v0v[r]));
+              if (has_x) p.x_out[gi] = cur;
+              if (has_out) ob[r * nx] = o;
+              if (has_part) dot = FMA ? fma(o, v0v[r], dot) : __dadd_rn(dot, __dmul_rn(o, v0v[r]));
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
                 dgj = fma(vj[r], v0v[r], dgj);
@@ -401,7 +413,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             if (MODE == kModeMV) {
               p.out[kofs + gi] = o;
             } else if (MODE == kModeMVR) {
-              if (p.v_norm_out) p.v_norm_out[kofs + gi] = cur;
+              if (has_vn) p.v_norm_out[kofs + gi] = cur;
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
               if (p.inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
                 if (k % nu == 0) {
@@ -416,9 +428,9 @@ __global__ void __launch_bounds__(kTmaThreads)
                 }
               }
             } else {
-              if (p.x_out) p.x_out[kofs + gi] = cur;
-              if (p.out) p.out[kofs + gi] = o;
-              if (p.partials) {
+              if (has_x) p.x_out[kofs + gi] = cur;
+              if (has_out) p.out[kofs + gi] = o;
+              if (has_part) {
                 dot = __dadd_rn(dot, __dmul_rn(o, v0v[r]));
               }
               if (wantj) {
@@ -439,7 +451,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
     }
   }
-  if (MODE == kModeIMV && p.partials) {
+  if (MODE == kModeIMV && has_part) {
     const double s = block_sum(dot);
     if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
   }
@@ -831,7 +843,7 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       break;
     case kModeMVR:
       if (d2) {
-        if (p.fma && !var && scaled && cfg_mvr == 0) {
+        if (p.fma && !var && scaled && cfg_mvr == 0 && p.v_norm_out) {
           rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                      bytes, cat);
           break;
@@ -852,7 +864,8 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       if (d2) {
         if (gather) {
           PMK_RUN(kModeIMV, 2, 4, 3, true);
-        } else if (p.fma && !var && !scaled && cfg_imv == 0) {
+        } else if (p.fma && !var && !scaled && cfg_imv == 0 && p.out && !p.x_out && p.partials &&
+                   p.v0) {
           rc = run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s, n_partials,
                                                                       bytes, cat);
         } else {
