@@ -92,6 +92,16 @@ __device__ __forceinline__ void fft_reg_dif(double2 (&a)[L]) {
   DifStage<L, Log2<L>::value>::run(a);
 }
 
+// compile-time bit reversal of B-bit indices (register subscripts)
+template <int B>
+struct ConstBrev {
+  static constexpr __host__ __device__ int of(int v) {
+    int r = 0;
+    for (int b = 0; b < B; ++b) r |= ((v >> b) & 1) << (B - 1 - b);
+    return r;
+  }
+};
+
 __device__ __forceinline__ int brev_bits(int v, int bits) {
   return bits ? (int)(__brev((unsigned)v) >> (32 - bits)) : 0;
 }
@@ -142,19 +152,31 @@ __device__ __forceinline__ void dst_group(Get get, Put put, double2 *buf, const 
     for (int q = 0; q < N2; ++q) c[r][q] = buf[k1 * (N2 + 1) + q];
     fft_reg_dif<N2>(c[r]);  // c[r][i] = C[k1][k2 = bitrev(i)]
   }
-  __syncwarp();
-  // W_k, k = k1 + N1 k2, back to the buffer in natural order
+  // Unpack X_p = [c (a_r - b_r) + s (a_i + b_i) - (a_i - b_i)] / 4 with
+  // A = W_p, B = W_{N-p}.  Lane n2 holds W_k for k = k1 + N1 k2, k1 = n2 +
+  // N2 r (register c[r][bitrev(k2)]); W_{N-p} sits in lane (N2 - n2) mod N2
+  // at (r', k2') = (R-1-r, N2-1-k2), or for lane 0 at (R-r mod R, ...) in its
+  // own registers -- a register shuffle instead of a shared-memory round trip.
+  constexpr int RR = N1 / N2;
+  const int src = (threadIdx.x & 31) - n2 + ((N2 - n2) & (N2 - 1));
 #pragma unroll
-  for (int r = 0; r < N1 / N2; ++r) {
-    const int k1 = n2 + N2 * r;
+  for (int r = 0; r < RR; ++r) {
 #pragma unroll
-    for (int i = 0; i < N2; ++i) buf[k1 + N1 * brev_bits(i, LG2)] = c[r][i];
-  }
-  __syncwarp();
-  // unpack X_p = [c (a_r - b_r) + s (a_i + b_i) - (a_i - b_i)] / 4
-  for (int p = n2 + 1; p < N; p += N2) {
-    const double2 A = buf[p], B = buf[N - p], cs = post[p];
-    put(p, 0.25 * (cs.x * (A.x - B.x) + cs.y * (A.y + B.y) - (A.y - B.y)));
+    for (int i = 0; i < N2; ++i) {
+      const int k2 = ConstBrev<LG2>::of(i);
+      const int ib = ConstBrev<LG2>::of(N2 - 1 - k2);   // partner register, lanes != 0
+      const int r0 = (r == 0) ? 0 : RR - r;              // lane 0: own registers
+      const int i0 = ConstBrev<LG2>::of((r == 0) ? ((N2 - k2) & (N2 - 1)) : N2 - 1 - k2);
+      double2 B;
+      B.x = __shfl_sync(0xffffffffu, c[RR - 1 - r][ib].x, src);
+      B.y = __shfl_sync(0xffffffffu, c[RR - 1 - r][ib].y, src);
+      if (n2 == 0) B = c[r0][i0];
+      const int p = n2 + N2 * r + N1 * k2;
+      if (p != 0) {
+        const double2 A = c[r][i], cs = post[p];
+        put(p, 0.25 * (cs.x * (A.x - B.x) + cs.y * (A.y + B.y) - (A.y - B.y)));
+      }
+    }
   }
   __syncwarp();
 }
