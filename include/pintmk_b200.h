@@ -121,8 +121,8 @@ typedef struct pmk_coarse {
   int32_t kind;
   int32_t dim, nx, ny, n_steps;
   const uint8_t *dropped; /* device [n_steps+1] or NULL (exact chain) */
-  const double *sx;       /* DST: [nx][nx] */
-  const double *sy;       /* DST: [ny][ny] (dim 2) */
+  const double *sx;       /* DST GEMM path: [nx][nx] (unused, may be NULL, with fft_x) */
+  const double *sy;       /* DST GEMM path: [ny][ny] (dim 2) */
   const double *delta;    /* DST: [m] eigenvalues of D */
   const double *beta;     /* DST: [m] eigenvalues of C */
   const double *dinv;     /* DENSE: [m][m] */

@@ -76,9 +76,26 @@ class StencilTable:
         self.constant = constant
         self.consts = consts
 
+    @classmethod
+    def from_constants(cls, consts, nx: int, ny: int) -> "StencilTable":
+        """Constant stencil (S, W, C, E, N) on an nx x ny grid, without a
+        matrix (the closed-form operators of pristine levels)."""
+        t = cls.__new__(cls)
+        t.nx, t.ny, t.m = nx, ny, nx * ny
+        t._dev = None
+        t._coef = None
+        t._lazy = None
+        t.constant = True
+        t.consts = np.asarray(consts, dtype=np.float64)
+        exists = t._full_pattern(nx, ny)[4]
+        t._exists = exists
+        return t
+
     @property
     def coef(self) -> np.ndarray:
         """(5, m) per-point coefficients (zeros where a neighbour is absent)."""
+        if self._coef is None and self._lazy is None:
+            self._coef = np.where(self._exists, self.consts[:, None], 0.0)
         if self._coef is None:
             self._coef = self._build_coef(*self._lazy)
         return self._coef
@@ -194,6 +211,24 @@ class SpectralInfo:
         self.a_dt = float(a_dt)
         self.b_dt = float(b_dt)
 
+    def stencils(self, dim: int) -> tuple[np.ndarray, np.ndarray]:
+        """(S, W, C, E, N) constants of diag and sub, equal bit for bit to the
+        entries scipy produces for ``eye - a_dt * A`` and ``eye + b_dt * A``
+        (spatial.py build_laplacian, solver.py _coarse_system_from): A's
+        off-diagonal entries are factor * 1, its diagonal factor * (-2 per
+        direction); a_dt * A rounds each entry once, the identity update once
+        more on the diagonal only.  Both blocks are symmetric, so these are
+        also the right-product (transposed) stencils."""
+        f = self.factor
+        ac = f * (-4.0 if dim == 2 else -2.0)
+        d_off, s_off = -(self.a_dt * f), self.b_dt * f
+        d_c, s_c = 1.0 - self.a_dt * ac, 1.0 + self.b_dt * ac
+        if dim == 2:
+            return (np.array([d_off, d_off, d_c, d_off, d_off]),
+                    np.array([s_off, s_off, s_c, s_off, s_off]))
+        return (np.array([0.0, d_off, d_c, d_off, 0.0]),
+                np.array([0.0, s_off, s_c, s_off, 0.0]))
+
 
 class CoarseSolver:
     """Device tables of the block forward substitution of one level
@@ -240,15 +275,17 @@ class CoarseSolver:
                 d.fft_scale = scale
             delta = 1.0 - spectral.a_dt * lam
             beta = 1.0 + spectral.b_dt * lam
-            sx = torch.from_numpy(dst_matrix(self.nx)).cuda()
-            tabs = [sx, torch.from_numpy(delta).cuda(), torch.from_numpy(beta).cuda()]
-            d.sx = sx.data_ptr()
-            if self.ny > 1:
-                sy = torch.from_numpy(dst_matrix(self.ny)).cuda()
-                tabs.append(sy)
-                d.sy = sy.data_ptr()
-            d.delta = tabs[1].data_ptr()
-            d.beta = tabs[2].data_ptr()
+            tabs = [torch.from_numpy(delta).cuda(), torch.from_numpy(beta).cuda()]
+            d.delta = tabs[0].data_ptr()
+            d.beta = tabs[1].data_ptr()
+            if not use_fft:  # dense sine matrices only for the GEMM transforms
+                sx = torch.from_numpy(dst_matrix(self.nx)).cuda()
+                tabs.append(sx)
+                d.sx = sx.data_ptr()
+                if self.ny > 1:
+                    sy = torch.from_numpy(dst_matrix(self.ny)).cuda()
+                    tabs.append(sy)
+                    d.sy = sy.data_ptr()
             self._keep += tabs
             self.work0 = torch.empty(self.N, dtype=torch.float64, device="cuda")
             # 2-D: second transform buffer; 1-D: chunked-recurrence scratch

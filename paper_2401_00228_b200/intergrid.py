@@ -298,5 +298,6 @@ def perturb_decouple(cs: CoarseSystem, n_cgs: int) -> CoarseSystem:
         raise ValueError(f"n_cgs must be in [1, {cs.n_steps + 1}]")
     chunks = np.array_split(np.arange(1, cs.n_steps + 1), min(n_cgs, cs.n_steps))
     dropped = tuple(int(c[0]) for c in chunks if len(c))
-    return CoarseSystem(diag=cs.diag, sub=cs.sub, n_steps=cs.n_steps, provenance="perturbed",
+    d_src, s_src = cs.block_sources()
+    return CoarseSystem(diag=d_src, sub=s_src, n_steps=cs.n_steps, provenance="perturbed",
                         dropped=dropped, grid=cs.grid, dim=cs.dim, spectral=cs.spectral)

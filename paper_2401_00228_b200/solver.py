@@ -174,13 +174,22 @@ class LevelHierarchy:
 def _coarse_system_from(spatial_matrix, implicit_weight, dt, n_steps, grid, dim,
                         laplace_factor) -> CoarseSystem:
     """D = I - a dt A, B = I + (1-a) dt A (reference solver.py:105-110)."""
-    eye = sp.identity(spatial_matrix.shape[0], format="csr")
-    diag = (eye - implicit_weight * dt * spatial_matrix).tocsr()
-    sub = (eye + (1.0 - implicit_weight) * dt * spatial_matrix).tocsr()
+    def diag():
+        eye = sp.identity(spatial_matrix.shape[0], format="csr")
+        return (eye - implicit_weight * dt * spatial_matrix).tocsr()
+
+    def sub():
+        eye = sp.identity(spatial_matrix.shape[0], format="csr")
+        return (eye + (1.0 - implicit_weight) * dt * spatial_matrix).tocsr()
+
     spectral = None
     if laplace_factor is not None:
+        # pristine level: the device takes the closed-form stencils; the
+        # scipy blocks are assembled only if a caller asks for them
         spectral = SpectralInfo(laplace_factor, implicit_weight * dt,
                                 (1.0 - implicit_weight) * dt)
+    else:
+        diag, sub = diag(), sub()
     return CoarseSystem(diag=diag, sub=sub, n_steps=n_steps, provenance="closed_form",
                         grid=grid, dim=dim, spectral=spectral)
 

@@ -21,7 +21,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from ._device import CoarseSolver, SpectralInfo, StencilTable, dropped_mask
-from .spatial import SpatialOperator
+from .spatial import SpatialOperator, laplacian_stencil, stencil_csr
 
 
 @dataclass
@@ -82,12 +82,34 @@ class StepOperators:
 
 def build_step_operators(op: SpatialOperator, cfg: ThetaSchemeConfig) -> StepOperators:
     """phi = I + (1-theta) dt A, psi = I - theta dt A (reference stepper.py:56-63)."""
-    eye = sp.identity(op.n, format="csr")
-    phi = (eye + (1.0 - cfg.theta) * cfg.delta_t * op.matrix).tocsr()
-    psi = (eye - cfg.theta * cfg.delta_t * op.matrix).tocsr()
+    if _is_pristine(op):
+        # closed form, entry for entry scipy's eye -/+ s * A
+        # (tests/test_host.py::test_direct_csr_assembly_bitwise)
+        spec = SpectralInfo(op.tau / op.delta_x**2, cfg.theta * cfg.delta_t,
+                            (1.0 - cfg.theta) * cfg.delta_t)
+        d, b = spec.stencils(op.dim)
+        psi = stencil_csr(op.n_x, op.n_y, d)
+        phi = stencil_csr(op.n_x, op.n_y, b)
+    else:
+        eye = sp.identity(op.n, format="csr")
+        phi = (eye + (1.0 - cfg.theta) * cfg.delta_t * op.matrix).tocsr()
+        psi = (eye - cfg.theta * cfg.delta_t * op.matrix).tocsr()
     ops = StepOperators(phi=phi, psi=psi, psi_factorization=None, spatial=op, config=cfg)
     ops.psi_factorization = _LazyDiagSolve(ops)
     return ops
+
+
+def _is_pristine(op: SpatialOperator) -> bool:
+    """op.matrix is build_laplacian's operator (checked on the entries of the
+    cached pattern: O(nnz) compares, no sparse arithmetic)."""
+    a = op.matrix
+    if not (sp.isspmatrix_csr(a) and a.shape == (op.n, op.n) and a.has_sorted_indices):
+        return False
+    _, _, slots, _, _, _, typed = StencilTable._full_pattern(op.n_x, op.n_y)
+    ip, ix = typed.get(a.indices.dtype, typed[np.dtype(np.int64)])
+    vals = laplacian_stencil(op.dim, op.tau / op.delta_x**2)
+    return (a.nnz == ix.size and np.array_equal(a.indptr, ip) and np.array_equal(a.indices, ix)
+            and np.array_equal(a.data, vals[slots]))
 
 
 def _to_device(v):
@@ -120,10 +142,16 @@ class BlockBidiagonalSystem:
     def __init__(self, diag: sp.csr_matrix, sub: sp.csr_matrix, n_steps: int,
                  dropped: tuple[int, ...] = (), grid: tuple[int, int] | None = None,
                  dim: int | None = None, spectral: SpectralInfo | None = None):
-        self.diag = sp.csr_matrix(diag)
-        self.sub = sp.csr_matrix(sub)
+        # diag / sub may also be zero-argument callables (internal: the
+        # closed-form blocks of pristine levels are assembled only when a
+        # caller asks for the matrices; the device path uses `spectral`)
+        self._diag_src, self._sub_src = diag, sub
+        self._diag = None if callable(diag) else sp.csr_matrix(diag)
+        self._sub = None if callable(sub) else sp.csr_matrix(sub)
+        if self._diag is None and (grid is None or spectral is None):
+            raise ValueError("lazily built blocks need the grid and spectral info")
         self.n_steps = n_steps
-        self.n = self.diag.shape[0]
+        self.n = self._diag.shape[0] if self._diag is not None else grid[0] * grid[1]
         self.dropped = tuple(sorted(dropped))
         if grid is None:
             grid = (self.n, 1)
@@ -138,6 +166,23 @@ class BlockBidiagonalSystem:
         self._desc = None
         self._solver = None
         self._keep = []
+
+    @property
+    def diag(self) -> sp.csr_matrix:
+        if self._diag is None:
+            self._diag = sp.csr_matrix(self._diag_src())
+        return self._diag
+
+    @property
+    def sub(self) -> sp.csr_matrix:
+        if self._sub is None:
+            self._sub = sp.csr_matrix(self._sub_src())
+        return self._sub
+
+    def block_sources(self):
+        """(diag, sub) as given: matrices or their lazy builders."""
+        return (self._diag if self._diag is not None else self._diag_src,
+                self._sub if self._sub is not None else self._sub_src)
 
     # ---------------------------------------------------------- bookkeeping
     @property
@@ -167,8 +212,13 @@ class BlockBidiagonalSystem:
         if self._desc is None:
             torch = _lib.require_cuda()
             nx, ny = self.grid
-            p = StencilTable(self.diag.T, nx, ny)   # right-product: v @ D = D^T v
-            q = StencilTable(self.sub.T, nx, ny)
+            if self.spectral is not None:  # closed form, bitwise the matrices' entries
+                cp, cq = self.spectral.stencils(self.dim)
+                p = StencilTable.from_constants(cp, nx, ny)
+                q = StencilTable.from_constants(cq, nx, ny)
+            else:
+                p = StencilTable(self.diag.T, nx, ny)   # right-product: v @ D = D^T v
+                q = StencilTable(self.sub.T, nx, ny)
             d = _lib.LevelDesc()
             d.dim, d.nx, d.ny, d.n_steps = self.dim, nx, ny, self.n_steps
             d.diag_t = p.desc()
@@ -225,7 +275,7 @@ class BlockBidiagonalSystem:
         rows = dr.numel() // self.n
         # A forward substitution whose every coupling is dropped applies D^{-1}
         # to each row; its row 0 is the identity, so prepend a zero row.
-        sys = BlockBidiagonalSystem(self.diag, self.sub, rows,
+        sys = BlockBidiagonalSystem(*self.block_sources(), rows,
                                     dropped=tuple(range(1, rows + 1)), grid=self.grid,
                                     dim=self.dim, spectral=self.spectral)
         torch = _lib.require_cuda()

@@ -120,6 +120,81 @@ def test_agglomerate_partition_matches_oracle():
         assert all(np.array_equal(a, b) for a, b in zip(g1, g2))
 
 
+@pytest.mark.parametrize("dim,nx,theta,dt,moves", [
+    (2, 255, 0.5, 1.6e-7 / 3, 4), (2, 63, 1.0, 2e-3, 2), (2, 15, 0.5, 1e-3, 3),
+    (1, 1023, 0.5, 3.05e-7, 3), (1, 63, 1.0, 7.8e-5, 1), (2, 127, 0.3, 1e-5, 3)])
+def test_closed_form_stencils_bitwise(dim, nx, theta, dt, moves):
+    """The closed-form stencils of pristine levels (SpectralInfo.stencils, used
+    instead of scanning the scipy blocks) equal the entries of the blocks the
+    reference's formulas produce, bit for bit, on the fine level and on every
+    time-coarsened level (a' = 1 - (1 - a)/nu, dt' = nu dt)."""
+    from paper_2401_00228_b200 import (ThetaSchemeConfig, build_laplacian,
+                                       build_step_operators)
+    from paper_2401_00228_b200._device import SpectralInfo, StencilTable
+    from paper_2401_00228_b200.solver import _coarse_system_from
+
+    op = build_laplacian(dim, nx, nx if dim == 2 else 1)
+    ops = build_step_operators(op, ThetaSchemeConfig(theta, dt, 64))
+    factor = op.tau / op.delta_x**2
+    ny = op.n_y
+    spec = SpectralInfo(factor, theta * dt, (1.0 - theta) * dt)
+    def same(mat, want):
+        # per-point coefficients (theta = 1 makes phi = I: scipy drops the
+        # zero neighbours, the closed form keeps them as 0.0 -- same products)
+        got = StencilTable(sp.csr_matrix(mat).T, nx, ny)
+        ref = StencilTable.from_constants(want, nx, ny)
+        assert np.array_equal(got.coef, ref.coef)
+        if got.constant:
+            assert np.array_equal(got.consts, want)
+
+    for mat, want in zip((ops.psi, ops.phi), spec.stencils(dim)):
+        same(mat, want)
+    a, h = theta, dt
+    for _ in range(moves):
+        a, h = 1.0 - (1.0 - a) / 2, 2 * h
+        cs = _coarse_system_from(op.matrix, a, h, 8, (nx, ny), dim, factor)
+        assert cs._diag is None  # not assembled by construction
+        for mat, want in zip((cs.diag, cs.sub), cs.spectral.stencils(dim)):
+            same(mat, want)
+
+
+@pytest.mark.parametrize("dim,nx,ny,tau,L,theta,dt", [
+    (2, 255, 255, 1.0, 1.0, 0.5, 1.6e-7), (2, 63, 17, 0.7, 2.0, 1.0, 1e-3),
+    (1, 1023, 1, 1.0, 1.0, 0.5, 3e-7), (1, 17, 1, 2.5, 1.0, 0.0, 1e-2), (2, 1, 1, 1.0, 1.0, 0.5, .1),
+    (2, 4, 6, 1.0, 1.0, 0.25, 2e-3), (2, 15, 9, 0.7, 2.0, 1.0, 1e-3), (1, 7, 1, 1.0, 1.0, 1.0, .1)])
+def test_direct_csr_assembly_bitwise(dim, nx, ny, tau, L, theta, dt):
+    """build_laplacian / build_step_operators assemble the CSR arrays directly;
+    they equal (indptr, indices, data, dtypes) scipy's kron / identity /
+    scalar-product assembly of the reference's formulas (spatial.py:37-72,
+    stepper.py:56-63), including the zero entries scipy drops (theta = 1
+    gives phi = I, theta = 0 psi = I)."""
+    from paper_2401_00228_b200 import (ThetaSchemeConfig, build_laplacian,
+                                       build_step_operators)
+
+    op = build_laplacian(dim, nx, ny, tau=tau, domain_length=L)
+    h = L / (nx + 1)
+    factor = tau / h**2
+    d2 = sp.diags([np.ones(nx - 1), np.full(nx, -2.0), np.ones(nx - 1)], [-1, 0, 1],
+                  format="csr")
+    if dim == 1:
+        ref = (factor * d2).tocsr()
+    else:
+        dy = sp.diags([np.ones(ny - 1), np.full(ny, -2.0), np.ones(ny - 1)], [-1, 0, 1],
+                      format="csr")
+        ref = (factor * (sp.kron(sp.identity(ny), d2) + sp.kron(dy, sp.identity(nx)))).tocsr()
+
+    def same(a, b):
+        assert a.shape == b.shape and a.indices.dtype == b.indices.dtype
+        assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
+        assert np.array_equal(a.data, b.data)
+
+    same(op.matrix, ref)
+    ops = build_step_operators(op, ThetaSchemeConfig(theta, dt, 8))
+    eye = sp.identity(op.n, format="csr")
+    same(ops.phi, (eye + (1.0 - theta) * dt * ref).tocsr())
+    same(ops.psi, (eye - theta * dt * ref).tocsr())
+
+
 def test_hierarchy_bookkeeping_host_only():
     """Level moves / weights / budgets without touching the device."""
     from paper_2401_00228_b200 import solver as S

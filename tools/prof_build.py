@@ -35,4 +35,5 @@ pr = cProfile.Profile()
 pr.enable()
 h = build()
 pr.disable()
-pstats.Stats(pr).sort_stats("tottime").print_stats(int(sys.argv[2]) if len(sys.argv) > 2 else 25)
+pstats.Stats(pr).sort_stats(os.environ.get("PROF_SORT", "tottime")).print_stats(
+    int(sys.argv[2]) if len(sys.argv) > 2 else 25)
