@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   const bool has_x = kSolver ? false : (p.x_out != nullptr);
   const bool has_part = kSolver ? (MODE == kModeIMV) : (p.partials != nullptr);
   const bool has_vn = kSolver ? (MODE == kModeMVR) : (p.v_norm_out != nullptr);
+  const bool has_drop = kSolver ? false : (p.dropped != nullptr);
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     }
     int Kc = (kstart == 0) ? 0 : (kstart - 1) / nu + 1;
     int posc = (kstart == 0) ? nu - 1 : (kstart - 1) - (Kc - 1) * nu;
-    int dnext = (p.dropped && kstart < ke) ? p.dropped[kstart] : 0;
+    int dnext = (has_drop && kstart < ke) ? p.dropped[kstart] : 0;
     for (int i = 0; i < nsl; ++i, ++it) {
       // ---- per-slice uniform quantities
       const int k = kstart + i;
@@ -249,7 +250,10 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
       // dropped coupling of k: loaded one slice ahead, off the critical path
       const bool drop = dnext != 0;
-      if (p.dropped && k + 1 < ke) dnext = p.dropped[k + 1];
+      // (a predicated-off load still holds its scoreboard until the memory
+      // pipe retires it, and shares it with the v_0 prefetch: solver
+      // launches have no dropped rows and skip the load entirely)
+      if (has_drop && k + 1 < ke) dnext = p.dropped[k + 1];
       const int pk = (int)(((int64_t)k * m + boxx) & 1);  // row parity shifts (issue())
       const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
       const int64_t kofs = (int64_t)k * m;
@@ -843,7 +847,7 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       break;
     case kModeMVR:
       if (d2) {
-        if (p.fma && !var && scaled && cfg_mvr == 0 && p.v_norm_out) {
+        if (p.fma && !var && scaled && cfg_mvr == 0 && p.v_norm_out && !p.dropped) {
           rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                      bytes, cat);
           break;
@@ -865,7 +869,7 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
         if (gather) {
           PMK_RUN(kModeIMV, 2, 4, 3, true);
         } else if (p.fma && !var && !scaled && cfg_imv == 0 && p.out && !p.x_out && p.partials &&
-                   p.v0) {
+                   p.v0 && !p.dropped) {
           rc = run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s, n_partials,
                                                                       bytes, cat);
         } else {
