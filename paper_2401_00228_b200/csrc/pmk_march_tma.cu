@@ -220,7 +220,13 @@ __global__ void __launch_bounds__(kTmaThreads)
     // tile whose rows and row neighbours all exist take the mask-free variant
     // of the stencil pass below (same operations, no neighbour selects).
     const bool tile_interior = DIM == 2 && (R % 2 == 0) && rlo == 0 && y0 + R <= ny - 1;
-    const bool warp_fast = __all_sync(0xffffffffu, tile_interior && xin && hw && he);
+    // In-solver (FMA) launches take the fused pass on every warp of an interior
+    // tile, zeroing the absent W/E neighbours of the first/last column (their
+    // products then add +-0) and masking the stores of columns past the grid:
+    // no warp of the tile runs the slower masked variant while the others wait
+    // for it at the slice barriers.
+    const bool warp_fast =
+        FMA ? tile_interior : __all_sync(0xffffffffu, tile_interior && xin && hw && he);
     double v0next[RO];
     if (MODE == kModeIMV && has_part) {
       const int kf = (kb > kstart) ? kb : kstart;  // first non-prime slice
@@ -312,7 +318,8 @@ __global__ void __launch_bounds__(kTmaThreads)
         for (int r = 0; r < RO; ++r) {
           const double *row = col + (r + 1) * kBox + (((r + 1) & 1) ? sh1 : sh0);
           const double dn = col[(r + 2) * kBox + (((r + 2) & 1) ? sh1 : sh0)];
-          const double lf = row[-1], rt = row[1];
+          const double lf = (FMA && !hw) ? 0.0 : row[-1];
+          const double rt = (FMA && !he) ? 0.0 : row[1];
           Coef5 a, b;
           if (VAR) {
             a = coef_at(p.P, gx0 + r * nx, m);
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(kTmaThreads)
                                      __dmul_rn(b.e, rt)),
                            __dmul_rn(b.n, dn));
           }
-          if (!prime) {
+          if (!prime && (!FMA || xin)) {
             const double o = __dsub_rn(Pu, qprev[r]);
             const int64_t gi = kofs + gx0 + r * nx;
             if (MODE == kModeMV) {
