@@ -147,6 +147,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   const bool has_part = kSolver ? (MODE == kModeIMV) : (p.partials != nullptr);
   const bool has_vn = kSolver ? (MODE == kModeMVR) : (p.v_norm_out != nullptr);
   const bool has_drop = kSolver ? false : (p.dropped != nullptr);
+  // j = 0 (v is v_0): <w, v_0> takes the staged input itself, no v_0 stream
+  const bool v0_self = kPj && p.v0 == p.v;
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -228,7 +230,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     const bool warp_fast =
         FMA ? tile_interior : __all_sync(0xffffffffu, tile_interior && xin && hw && he);
     double v0next[RO];
-    if (MODE == kModeIMV && has_part) {
+    if (MODE == kModeIMV && has_part && !v0_self) {
       const int kf = (kb > kstart) ? kb : kstart;  // first non-prime slice
 #pragma unroll
       for (int r = 0; r < RO; ++r)
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       double vj[RO];  // the staged input at this thread's outputs (pj dots)
 #pragma unroll
       for (int r = 0; r < RO; ++r) vj[r] = 0.0;
-      if (MODE == kModeIMV && has_part) {
+      if (MODE == kModeIMV && has_part && !v0_self) {
 #pragma unroll
         for (int r = 0; r < RO; ++r) v0v[r] = v0next[r];
         const int kn = k + 1;  // prefetch the next slice of this item
@@ -365,10 +367,11 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (has_x) p.x_out[gi] = cur;
               if (has_out) ob[r * nx] = o;
-              if (has_part) dot = FMA ? fma(o, v0v[r], dot) : __dadd_rn(dot, __dmul_rn(o, v0v[r]));
+              const double v0r = v0_self ? vj[r] : v0v[r];
+              if (has_part) dot = FMA ? fma(o, v0r, dot) : __dadd_rn(dot, __dmul_rn(o, v0r));
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
-                dgj = fma(vj[r], v0v[r], dgj);
+                dgj = fma(vj[r], v0r, dgj);
               }
             }
           }
@@ -441,12 +444,13 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (has_x) p.x_out[kofs + gi] = cur;
               if (has_out) p.out[kofs + gi] = o;
+              const double v0r = v0_self ? vj[r] : v0v[r];
               if (has_part) {
-                dot = __dadd_rn(dot, __dmul_rn(o, v0v[r]));
+                dot = __dadd_rn(dot, __dmul_rn(o, v0r));
               }
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
-                dgj = fma(vj[r], v0v[r], dgj);
+                dgj = fma(vj[r], v0r, dgj);
               }
             }
           }
