@@ -147,6 +147,13 @@ __global__ void __launch_bounds__(kTmaThreads)
   const bool has_part = kSolver ? (MODE == kModeIMV) : (p.partials != nullptr);
   const bool has_vn = kSolver ? (MODE == kModeMVR) : (p.v_norm_out != nullptr);
   const bool has_drop = kSolver ? false : (p.dropped != nullptr);
+  // In-solver K-MVR works on the raw (unnormalised) staged values: the
+  // operator is linear, so A v - mu v = RN(1/h) (A raw - mu raw) up to
+  // rounding; only the stored outputs are scaled (v itself is stored as
+  // RN(raw * RN(1/h)), exactly the pre-pass value).  No pre-pass, and one
+  // block barrier per slice fewer.
+  constexpr bool kLazy = FMA && MODE == kModeMVR && SCALED;
+  const double osc = kLazy ? vrcp : 1.0;
   // j = 0 (v is v_0): <w, v_0> takes the staged input itself, no v_0 stream
   const bool v0_self = kPj && p.v0 == p.v;
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
@@ -282,7 +289,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
       mbar_wait(&bars[stage], (it / S) & 1);
       // ---- pre-pass: u = v / scale  or  u = v - Z vt, once per element
-      if ((SCALED || MODE == kModeIMV) && pin) {
+      if (((SCALED && !kLazy) || MODE == kModeIMV) && pin) {
         const double *vtk = GATHER ? p.vt + (int64_t)K * p.m_coarse : nullptr;
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           *cell = u;
         }
       }
-      if (SCALED || MODE == kModeIMV) __syncthreads();
+      if ((SCALED && !kLazy) || MODE == kModeIMV) __syncthreads();
       // ---- stencil pass, mask-free variant: every neighbour exists, k >= 1,
       // no dropped coupling.  Tile rows start at even y0 (R even) and box row
       // r holds grid row y0 - 1 + r, odd for even r: its parity shift
@@ -350,18 +357,20 @@ __global__ void __launch_bounds__(kTmaThreads)
             if (MODE == kModeMV) {
               p.out[gi] = o;
             } else if (MODE == kModeMVR) {
-              if (wn) ob[r * nx] = cur;
+              if (wn) ob[r * nx] = kLazy ? __dmul_rn(cur, osc) : cur;
               const double sval = FMA ? fma(-p.mu, cur, o) : __dsub_rn(o, __dmul_rn(p.mu, cur));
               if (inj) {
                 if (k % nu == 0) {
-                  p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sval;
-                  vsq = __dadd_rn(vsq, __dmul_rn(sval, sval));
+                  const double sv = kLazy ? __dmul_rn(sval, osc) : sval;
+                  p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sv;
+                  vsq = __dadd_rn(vsq, __dmul_rn(sv, sv));
                 }
               } else {
                 acc[r] = opens ? sval : __dadd_rn(acc[r], sval);
                 if (closes) {
-                  hb[r * nx] = acc[r];
-                  vsq = __dadd_rn(vsq, __dmul_rn(acc[r], acc[r]));
+                  const double av = kLazy ? __dmul_rn(acc[r], osc) : acc[r];
+                  hb[r * nx] = av;
+                  vsq = __dadd_rn(vsq, __dmul_rn(av, av));
                 }
               }
             } else {
@@ -427,18 +436,20 @@ __global__ void __launch_bounds__(kTmaThreads)
             if (MODE == kModeMV) {
               p.out[kofs + gi] = o;
             } else if (MODE == kModeMVR) {
-              if (has_vn) p.v_norm_out[kofs + gi] = cur;
+              if (has_vn) p.v_norm_out[kofs + gi] = kLazy ? __dmul_rn(cur, osc) : cur;
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
               if (p.inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
                 if (k % nu == 0) {
-                  p.vh[(int64_t)(k / nu) * m + gi] = sval;
-                  vsq = __dadd_rn(vsq, __dmul_rn(sval, sval));
+                  const double sv = kLazy ? __dmul_rn(sval, osc) : sval;
+                  p.vh[(int64_t)(k / nu) * m + gi] = sv;
+                  vsq = __dadd_rn(vsq, __dmul_rn(sv, sv));
                 }
               } else {
                 acc[r] = (pos == 0 || k == 0) ? sval : __dadd_rn(acc[r], sval);
                 if (pos == nu - 1) {
-                  p.vh[(int64_t)K * m + gi] = acc[r];
-                  vsq = __dadd_rn(vsq, __dmul_rn(acc[r], acc[r]));
+                  const double av = kLazy ? __dmul_rn(acc[r], osc) : acc[r];
+                  p.vh[(int64_t)K * m + gi] = av;
+                  vsq = __dadd_rn(vsq, __dmul_rn(av, av));
                 }
               }
             } else {
