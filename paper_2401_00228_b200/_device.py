@@ -257,10 +257,7 @@ class CoarseSolver:
                        and (self.ny == 1 or (taby is not None and self.ny + 1 <= 512)))
             if self.ny > 1:
                 ey = dst_eigenvalues_1d(self.ny)
-                if use_fft:  # FFT path: modes [p][q] (x-mode slow, pmk_coarse.cu)
-                    lam = spectral.factor * (ex[:, None] + ey[None, :])
-                else:        # GEMM path: S_y X S_x, modes [q][p]
-                    lam = spectral.factor * (ey[:, None] + ex[None, :])
+                lam = spectral.factor * (ey[:, None] + ex[None, :])  # y-mode slow
             else:
                 lam = spectral.factor * ex[None, :]
             lam = lam.ravel()

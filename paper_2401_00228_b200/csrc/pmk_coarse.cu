@@ -408,11 +408,10 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       if (rc) return rc;
     } else {
       PMK_RETURN_IF(!C.fft_y || !C.work1, PMK_ERR_ARG);
-      // x (written transposed, [k][p][y]), y (contiguous rows -> modes
-      // [k][p][q], p slow), recurrence, y, x (read transposed)
-      rc = launch_dst_rows_t(rhs, C.work0, nx, ny, rows, C.fft_x, 0, live, s);
+      // x then y (modes [k][q][p], q slow), recurrence, y then x
+      rc = launch_dst_rows(rhs, C.work0, nx, (int64_t)rows * ny, C.fft_x, live, s);
       if (rc) return rc;
-      rc = launch_dst_rows(C.work0, C.work1, ny, (int64_t)rows * nx, C.fft_y, live, s);
+      rc = launch_dst_cols(C.work0, C.work1, nx, ny, rows, C.fft_y, live, s);
       if (rc) return rc;
       {
         prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
@@ -421,9 +420,9 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
                                                              C.fft_scale, live);
       }
       PMK_LAUNCH_CHECK();
-      rc = launch_dst_rows(C.work1, C.work0, ny, (int64_t)rows * nx, C.fft_y, live, s);
+      rc = launch_dst_cols(C.work1, C.work0, nx, ny, rows, C.fft_y, live, s);
       if (rc) return rc;
-      rc = launch_dst_rows_t(C.work0, out, nx, ny, rows, C.fft_x, 1, live, s);
+      rc = launch_dst_rows(C.work0, out, nx, (int64_t)rows * ny, C.fft_x, live, s);
       if (rc) return rc;
     }
     {

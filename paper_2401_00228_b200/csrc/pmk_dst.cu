@@ -225,69 +225,6 @@ __global__ void __launch_bounds__(32 * kDstWarps)
   }
 }
 
-// x-direction transform of 2-D slices with a transposed side, so that the
-// y-direction transform is a contiguous-row transform too (no column-tile
-// kernel).  A CTA owns RB consecutive grid rows (rows of (slice k, y) order):
-//   TOUT: in [k][y][x] rows -> out [k][p][y]: outputs staged in shared
-//         memory, written as runs of RB consecutive y per mode p;
-//   TIN:  in [k][p][y] -> out [k][y][x] rows: the RB input rows gathered
-//         through shared memory (runs of RB consecutive y per p) first.
-template <int LOGN, bool TIN>
-__global__ void __launch_bounds__(32 * kDstWarps)
-    dst_rows_t_kernel(const double *__restrict__ in, double *__restrict__ out, int64_t rows,
-                      int ny, const double2 *gtw2, const double2 *gpost, const int *live) {
-  if (!is_live(live)) return;
-  using P = Plan<LOGN>;
-  constexpr int N = P::N, n = N - 1;
-  constexpr int RB = kDstWarps * P::TPW;  // rows per CTA step
-  constexpr int SP = N + 1;               // staging row stride (conflict-free columns)
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double2 *tw2 = reinterpret_cast<double2 *>(smem_raw);
-  double2 *post = tw2 + N;
-  double2 *bufs = post + N;
-  double *stage = reinterpret_cast<double *>(bufs + kDstWarps * P::TPW * P::BS);  // [RB][SP]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = lane / P::N2, n2 = lane % P::N2;
-  const int jr = warp * P::TPW + h;  // this group's row within the step
-  double2 *buf = bufs + jr * P::BS;
-  load_tables<LOGN>(tw2, post, gtw2, gpost);
-  const int64_t m = (int64_t)n * ny;  // slice size
-  for (int64_t base = (int64_t)blockIdx.x * RB; base < rows; base += (int64_t)gridDim.x * RB) {
-    __syncthreads();  // tables loaded / previous step's stage consumed
-    if (TIN) {  // gather: stage[j][p] = in[k][p][y] for row base + j = (k, y)
-      for (int idx = threadIdx.x; idx < RB * n; idx += blockDim.x) {
-        const int j = idx % RB, q = idx / RB;
-        const int64_t r = base + j;
-        if (r < rows) {
-          const int64_t k = r / ny, y = r - k * ny;
-          stage[j * SP + q] = __ldg(in + k * m + (int64_t)q * ny + y);
-        }
-      }
-      __syncthreads();
-    }
-    const int64_t r = base + jr;
-    const bool ok = r < rows;
-    const double *x = TIN ? stage + jr * SP : in + (ok ? r : 0) * n;
-    double *y = TIN ? out + (ok ? r : 0) * n : stage + jr * SP;
-    dst_group<LOGN>([&](int j) { return ok ? (TIN ? x[j] : __ldg(x + j)) : 0.0; },
-                    [&](int pp, double v) {
-                      if (ok) y[pp - 1] = v;
-                    },
-                    buf, tw2, post, n2);
-    if (!TIN) {  // scatter: out[k][p][y] = stage[j][p]
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < RB * n; idx += blockDim.x) {
-        const int j = idx % RB, q = idx / RB;
-        const int64_t rr = base + j;
-        if (rr < rows) {
-          const int64_t k = rr / ny, yy = rr - k * ny;
-          out[k * m + (int64_t)q * ny + yy] = stage[j * SP + q];
-        }
-      }
-    }
-  }
-}
-
 template <int LOGN>
 __global__ void __launch_bounds__(32 * kDstWarps)
     dst_cols_kernel(const double *__restrict__ in, double *__restrict__ out, int nx, int slices,
@@ -417,34 +354,6 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
   return 0;
 }
 
-template <int LOGN, bool TIN>
-int run_dst_t(const double *in, double *out, int64_t rows, int ny, const double *tables,
-              const int *live, cudaStream_t s) {
-  using P = Plan<LOGN>;
-  constexpr int N = P::N;
-  constexpr int RB = kDstWarps * P::TPW;
-  const int rc0 = init_constants();
-  if (rc0) return rc0;
-  const size_t smem = (size_t)(2 * N + kDstWarps * P::TPW * P::BS) * sizeof(double2) +
-                      (size_t)RB * (N + 1) * sizeof(double);
-  auto kern = dst_rows_t_kernel<LOGN, TIN>;
-  static int occ = -1;
-  if (occ < 0) {
-    PMK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int b = 0;
-    PMK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kDstWarps, smem));
-    occ = b > 0 ? b : 1;
-  }
-  const int64_t need = (rows + RB - 1) / RB;
-  const int grid = (int)(need < (int64_t)occ * kSMs ? need : (int64_t)occ * kSMs);
-  const double elems = (double)rows * (N - 1);
-  prof::Scope scope(prof::kGemm, 16.0 * elems, rows * (5.0 * N * LOGN + 8.0 * N), s);
-  const double2 *tw2 = reinterpret_cast<const double2 *>(tables);
-  kern<<<grid, 32 * kDstWarps, smem, s>>>(in, out, rows, ny, tw2, tw2 + N, live);
-  PMK_LAUNCH_CHECK();
-  return 0;
-}
-
 int log2_exact(int n1) {
   int l = 0;
   while ((1 << l) < n1) ++l;
@@ -469,24 +378,6 @@ int launch_dst_rows(const double *in, double *out, int n, int64_t rows, const do
     case 9: return run_dst<9, false>(in, out, rows, 0, tables, live, s, rps, oss);
     case 10: return run_dst<10, false>(in, out, rows, 0, tables, live, s, rps, oss);
   }
-  return PMK_ERR_UNSUPPORTED;
-}
-
-// DST of every grid row of (slices, ny, nx) data (n = nx, n + 1 = 2^2 ..
-// 2^9) with the transposed side: transposed_in = 0 writes (slices, nx, ny),
-// 1 reads (slices, nx, ny) and writes (slices, ny, nx).
-int launch_dst_rows_t(const double *in, double *out, int n, int ny, int64_t slices,
-                      const double *tables, int transposed_in, const int *live,
-                      cudaStream_t s) {
-  const int64_t rows = slices * ny;
-#define PMK_T(L)                                                             \
-  case L:                                                                    \
-    return transposed_in ? run_dst_t<L, true>(in, out, rows, ny, tables, live, s) \
-                         : run_dst_t<L, false>(in, out, rows, ny, tables, live, s);
-  switch (log2_exact(n + 1)) {
-    PMK_T(2) PMK_T(3) PMK_T(4) PMK_T(5) PMK_T(6) PMK_T(7) PMK_T(8) PMK_T(9)
-  }
-#undef PMK_T
   return PMK_ERR_UNSUPPORTED;
 }
 

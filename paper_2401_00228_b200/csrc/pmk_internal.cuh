@@ -214,9 +214,6 @@ int mgrit_interpolate(const pmk_pair &P, const double *w, double *out, const int
                       cudaStream_t s);
 int launch_dst_cols(const double *in, double *out, int nx, int ny, int slices,
                     const double *tables, const int *live, cudaStream_t s);
-int launch_dst_rows_t(const double *in, double *out, int n, int ny, int64_t slices,
-                      const double *tables, int transposed_in, const int *live,
-                      cudaStream_t s);
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
                  cudaStream_t s);
 
