@@ -226,6 +226,14 @@ int pmk_fgmres_begin(pmk_hier *H, int32_t idx, const double *rhs,
                      int32_t max_iter, double tol, pmk_stream_t stream);
 int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *v_out,
                     double *w_next, double *child_out, pmk_stream_t stream);
+/* 1 when the solver keeps a lazy basis (the default ICWY path; PMK_LAZY=0
+ * or PMK_MGS=classic turn it off): step j then keeps its w_next as the raw
+ * basis vector j+1 (so w_next must be a fresh buffer every step; v_0 is the
+ * rhs itself), never writes a normalised copy unless v_out is non-NULL (it may
+ * be NULL), and every consumer uses RN(raw * RN(1/scale)) -- the values the
+ * normalised basis would hold.  0: v_out (required) receives v_j and w_next
+ * may be reused across steps. */
+int32_t pmk_lazy_basis(void);
 int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x,
                       pmk_stream_t stream);
 /* finish restricted to the time slices [row_begin, row_end) of x (row_begin a

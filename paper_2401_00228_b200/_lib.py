@@ -94,6 +94,7 @@ SIGNATURES = {
     "pmk_profile_end_levels": (c_int32, [POINTER(c_double), c_int32, POINTER(c_int32)]),
     "pmk_profile_category": (ctypes.c_char_p, [c_int32]),
     "pmk_launch_count": (c_int64, []),
+    "pmk_lazy_basis": (c_int32, []),
     "pmk_div_check": (c_int32, [c_void_p, c_double, c_int64, c_void_p, c_void_p]),
 }
 
@@ -205,3 +206,8 @@ def launch_count() -> int:
 
 def ptr(t) -> c_void_p:
     return c_void_p(0 if t is None else t.data_ptr())
+
+
+def lazy_basis() -> bool:
+    """True when the native solver keeps a lazy (raw) Krylov basis."""
+    return bool(load().pmk_lazy_basis())

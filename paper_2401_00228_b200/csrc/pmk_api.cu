@@ -207,6 +207,16 @@ bool classic_mgs() {
   return on;
 }
 
+// Lazy basis (KState::lazy; the ICWY path, PMK_LAZY=0 turns it off): no
+// normalisation pass writes v_j; every consumer scales the raw vector.
+bool lazy_basis() {
+  static const bool on = [] {
+    const char *e = getenv("PMK_LAZY");
+    return !classic_mgs() && !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // vh = Y^T (A v - mu v) ; optionally v_norm_out = v (normalised input)
 int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
            const double *v_scale, double *vh, double *scratch, double *v_norm_out,
@@ -296,7 +306,9 @@ int alloc_state(LevelRT &R, int cap) {
   d += cap + 1;
   h.hist = d;
   d += cap + 1;
-  d += cap + 1;  // spare
+  h.vrcp = d;
+  d += cap + 1;
+  h.lazy = lazy_basis() ? 1 : 0;
   R.partA = d;  // K-IMV <w, v_0>, then the pj block (<w, v_j>, <v_j, v_0>)
   d += 3 * kMaxPartials;
   R.partB = d;
@@ -435,19 +447,24 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
   PMK_RETURN_IF(j != (int)R.vt.size() || j >= R.cap, PMK_ERR_STATE);
-  PMK_RETURN_IF(!v_out || !w_next || !child_out, PMK_ERR_ARG);
+  const bool lazy = R.h_state.lazy != 0;
+  PMK_RETURN_IF((!lazy && !v_out) || !w_next || !child_out, PMK_ERR_ARG);
   PMK_RETURN_IF(w_next == R.rhs_cur || v_out == R.pending, PMK_ERR_ARG);
+  // lazy basis: w_next is kept as raw basis vector j+1 and may not be a
+  // buffer of the current basis (a fresh buffer per step)
+  for (const double *b : R.v) PMK_RETURN_IF(lazy && w_next == b, PMK_ERR_ARG);
   double *vh = child_rhs(H, idx);
   PMK_RETURN_IF(!vh, PMK_ERR_STATE);
   const int *live = live_ptr(R);
   const KState &K = R.h_state;
-  // apply_preconditioner (solver.py:336-359); the pass that reads the
-  // unnormalised basis vector also stores v_j = raw / scale.
-  // (in-solver normalisation by reciprocal multiply, <= 1 ulp; the
-  // classic mode keeps the reference's division)
+  // apply_preconditioner (solver.py:336-359) on v_j = raw / scale (in-solver
+  // normalisation by reciprocal multiply, <= 1 ulp; the classic mode keeps
+  // the reference's division).  Normalised basis: this pass also stores v_j
+  // into v_out.  Lazy basis: v_j stays raw (every consumer scales it); v_out,
+  // if given, still receives the normalised copy.
   int rc = mvr_into_child(H, idx, R.pending, K.vscale + j, v_out, live, s, classic_mgs());
   if (rc) return rc;
-  R.v.push_back(v_out);
+  R.v.push_back(lazy ? R.pending : v_out);
   if (R.P.mgrit) {
     // coarse solve into the pair's scratch, then ideal interpolation into the
     // iteration's (fine-size) child_out (intergrid.py:157-167)
@@ -467,8 +484,9 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     return !(e && e[0] == '0');
   }();
   double *pj = (j >= 1 && !classic_mgs() && pj_on) ? R.partA + kMaxPartials : nullptr;
-  rc = do_imv(R.L, R.P, v_out, nullptr, child_out, nullptr, w_next, R.v[0], nullptr, R.partA,
-              &np, live, s, !classic_mgs(), pj, &pj_done);
+  rc = do_imv(R.L, R.P, R.v[j], lazy ? K.vscale + j : nullptr, child_out, nullptr, w_next,
+              R.v[0], lazy ? K.vscale : nullptr, R.partA, &np, live, s, !classic_mgs(), pj,
+              &pj_done);
   if (rc) return rc;
   if (!classic_mgs()) {
     // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412);
@@ -561,8 +579,13 @@ int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaSt
                 PMK_ERR_STATE);
   int rc = fgmres_begin(H, idx, R.rhs, R.budget, 0.0, parent_live, s);
   if (rc) return rc;
+  const bool lazy = R.h_state.lazy != 0;
   for (int j = 0; j < R.budget; ++j) {
-    rc = fgmres_step(H, idx, j, R.v_slots[j], R.w_buf, R.child_out[j], s, j + 1 < R.budget);
+    // lazy basis: v_0 is the rhs, step j's w goes to slot j+1 (it is basis
+    // vector j+1), the last step's w only feeds ||w|| (w_buf)
+    double *w_next = (lazy && j + 1 < R.budget) ? R.v_slots[j + 1] : R.w_buf;
+    rc = fgmres_step(H, idx, j, lazy ? nullptr : R.v_slots[j], w_next, R.child_out[j], s,
+                     j + 1 < R.budget);
     if (rc) return rc;
   }
   return fgmres_finish(H, idx, x, s);
@@ -587,6 +610,8 @@ extern "C" {
 const char *pmk_version(void) { return "pintmk_b200 0.1 sm_100a"; }
 
 int64_t pmk_launch_count(void) { return g_launches.load(); }
+
+int32_t pmk_lazy_basis(void) { return lazy_basis() ? 1 : 0; }
 
 int pmk_div_check(const double *x, double d, int64_t n, double *out, pmk_stream_t stream) {
   PMK_RETURN_IF(!x || !out || n < 0, PMK_ERR_ARG);

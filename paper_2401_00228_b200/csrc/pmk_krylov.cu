@@ -111,6 +111,7 @@ __global__ void begin_kernel(KState *st, const double *partials, int n_partials,
     const double beta = sqrt(ss);
     st->beta = beta;
     st->vscale[0] = beta;
+    st->vrcp[0] = st->lazy ? __drcp_rn(beta) : 1.0;
     st->g[0] = beta;
     st->rel = 1.0;
     st->live = (beta == 0.0) ? 0 : 1;  // solver.py:382-383: zero rhs -> x = 0
@@ -379,20 +380,23 @@ __global__ void __launch_bounds__(1024)
     double x;
     if (d == 0) {
       x = warp_reduce_partials(c0p, n_c0);
-    } else if (d < j) {  // <w, v_d>, 1 <= d < j
+    } else if (d < j) {  // <w, v_d>, 1 <= d < j (dot pass: raw v_d)
       const int e = d - o;
       x = warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride + (e % kDotGroup) * n_gp, n_gp);
-    } else if (d == j) {  // <w, v_j>
+      x = __dmul_rn(x, st->vrcp[d]);
+    } else if (d == j) {  // <w, v_j> (K-IMV: scaled; dot pass: raw v_j)
       x = pj ? warp_reduce_partials(pj, n_c0)
-             : warp_reduce_partials(gp + (int64_t)2 * kDotGroup * n_gp, n_gp);
+             : __dmul_rn(warp_reduce_partials(gp + (int64_t)2 * kDotGroup * n_gp, n_gp),
+                         st->vrcp[j]);
     } else {  // <v_j, v_i>, i = d - j - 1
       const int i = d - j - 1;
       const int e = i - o;
       x = (pj && i == 0)
               ? warp_reduce_partials(pj + kMaxPartials, n_c0)
-              : warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride +
-                                         (kDotGroup + e % kDotGroup) * n_gp,
-                                     n_gp);
+              : __dmul_rn(warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride +
+                                                   (kDotGroup + e % kDotGroup) * n_gp,
+                                               n_gp),
+                          __dmul_rn(st->vrcp[j], st->vrcp[i]));
     }
     if (lane == 0) {
       if (d <= j)
@@ -434,8 +438,8 @@ __global__ void __launch_bounds__(kRedThreads)
   double hq[CNT];
   const double2 *c2[CNT];
 #pragma unroll
-  for (int q = 0; q < CNT; ++q) {
-    hq[q] = st->h[(int64_t)(i0 + q) * ld + j];
+  for (int q = 0; q < CNT; ++q) {  // (lazy basis: h_q v_q = (h_q vrcp_q) raw_q)
+    hq[q] = __dmul_rn(st->h[(int64_t)(i0 + q) * ld + j], st->vrcp[i0 + q]);
     c2[q] = reinterpret_cast<const double2 *>(V.v[q]);
   }
   double acc[1] = {0.0};
@@ -490,7 +494,8 @@ __global__ void __launch_bounds__(kRedThreads)
   if (!st->live) return;
   double hq[kGroup];
 #pragma unroll
-  for (int q = 0; q < kGroup; ++q) hq[q] = (q < count) ? st->h[(int64_t)(i0 + q) * ld + j] : 0.0;
+  for (int q = 0; q < kGroup; ++q)
+    hq[q] = (q < count) ? __dmul_rn(st->h[(int64_t)(i0 + q) * ld + j], st->vrcp[i0 + q]) : 0.0;
   double acc[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -519,7 +524,10 @@ __global__ void finish_col_kernel(KState *st, int ld, int j, const double *parti
   for (int l = 0; l <= j + 1; ++l) cn2 = __dadd_rn(cn2, __dmul_rn(h[l * ld + j], h[l * ld + j]));
   const double col_norm = sqrt(cn2);
   const bool breakdown = hn <= 1e-14 * fmax(col_norm, 1e-300);
-  if (!breakdown) st->vscale[j + 1] = hn;
+  if (!breakdown) {
+    st->vscale[j + 1] = hn;
+    st->vrcp[j + 1] = st->lazy ? __drcp_rn(hn) : 1.0;
+  }
   double *cs = st->cs, *sn = st->sn, *g = st->g;
   for (int l = 0; l < j; ++l) {
     const double a = h[l * ld + j], b = h[(l + 1) * ld + j];
@@ -579,7 +587,8 @@ __global__ void __launch_bounds__(256)
       double acc = (first == 0) ? 0.0 : x[e];
       for (int l = first; l < hi; ++l) {
         const int q = l - first;
-        const double xl = __dsub_rn(__ldg(a.v[q] + e), __ldg(a.vt[q] + ci));
+        const double vl = __dmul_rn(__ldg(a.v[q] + e), st->vrcp[l]);  // (lazy basis)
+        const double xl = __dsub_rn(vl, __ldg(a.vt[q] + ci));
         acc = __dadd_rn(acc, __dmul_rn(st->y[l], xl));
       }
       x[e] = acc;
@@ -603,9 +612,12 @@ __global__ void __launch_bounds__(256)
   const int n_iter = st->n_iter;
   if (first > 0 && first >= n_iter) return;
   const int hi = min(n_iter, first + CNT);
-  double y[CNT];
+  double y[CNT], sc[CNT];  // sc: lazy-basis scales (1 for a normalised basis)
 #pragma unroll
-  for (int q = 0; q < CNT; ++q) y[q] = (first + q < hi) ? st->y[first + q] : 0.0;
+  for (int q = 0; q < CNT; ++q) {
+    y[q] = (first + q < hi) ? st->y[first + q] : 0.0;
+    sc[q] = (first + q < hi) ? st->vrcp[first + q] : 1.0;
+  }
   const int chunk = 256 * U;
   const int n_coarse = rows / 2 + 1;  // K = 0 and the pairs (2K-1, 2K)
   for (int K = blockIdx.y; K < n_coarse; K += gridDim.y) {
@@ -638,8 +650,8 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int q = 0; q < CNT; ++q)
           if (first + q < hi) {
-            s0 = __dadd_rn(s0, __dmul_rn(y[q], __dsub_rn(v0[u][q], tt[u][q])));
-            s1 = __dadd_rn(s1, __dmul_rn(y[q], __dsub_rn(v1[u][q], tt[u][q])));
+            s0 = __dadd_rn(s0, __dmul_rn(y[q], __dsub_rn(__dmul_rn(v0[u][q], sc[q]), tt[u][q])));
+            s1 = __dadd_rn(s1, __dmul_rn(y[q], __dsub_rn(__dmul_rn(v1[u][q], sc[q]), tt[u][q])));
           }
         x[e0] = s0;
         if (two) x[e0 + m] = s1;

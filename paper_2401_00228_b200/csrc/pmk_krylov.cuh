@@ -14,6 +14,12 @@ struct KState {
   double *hraw;  // unrotated copy (keep_basis, tests)
   double *cs, *sn, *g, *y;
   double *vscale;  // vscale[l]: divisor of raw basis vector l (beta, h[l][l-1])
+  // Lazy basis (lazy = 1): basis vector l is stored raw (the rhs, or w of
+  // iteration l-1 after its orthogonalisation) and used as RN(raw * vrcp[l]),
+  // vrcp[l] = RN(1 / vscale[l]) -- the exact values an explicit normalisation
+  // pass would have stored.  lazy = 0: stored normalised, vrcp[l] = 1.
+  double *vrcp;
+  int lazy;
   double *hist;    // residual history rel_j
   double *gram;    // cap x cap, row i = <v_i, v_l>, l < i (ICWY MGS)
   double beta, rel;

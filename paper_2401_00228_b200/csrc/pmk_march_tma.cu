@@ -75,6 +75,13 @@ struct Coef5 {
   double s, w, c, e, n;
 };
 
+// Dropped-coupling flags are read a slice ahead through a pointer that is
+// always valid (stride 0 over a zero byte when the level has no dropped
+// rows), so the load is never predicated off: a predicated-off load keeps its
+// scoreboard until the memory pipe retires it, which stalled its consumer
+// behind every other load sharing that scoreboard.
+__device__ const uint8_t g_no_drop = 0;
+
 __device__ __forceinline__ Coef5 coef_at(const pmk_stencil &st, int64_t i, int m) {
   if (!st.var) return Coef5{st.c[0], st.c[1], st.c[2], st.c[3], st.c[4]};
   const double *c = st.coef;
@@ -145,8 +152,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   const bool has_out = kSolver ? (MODE != kModeMVR) : (p.out != nullptr);
   const bool has_x = kSolver ? false : (p.x_out != nullptr);
   const bool has_part = kSolver ? (MODE == kModeIMV) : (p.partials != nullptr);
-  const bool has_vn = kSolver ? (MODE == kModeMVR) : (p.v_norm_out != nullptr);
-  const bool has_drop = kSolver ? false : (p.dropped != nullptr);
+  // (K-MVR's normalised v is optional: with a lazy basis nobody stores it)
+  const bool has_vn = p.v_norm_out != nullptr;
+  const bool has_drop = !kSolver;  // (solver launches: no dropped rows, no load)
   // In-solver K-MVR works on the raw (unnormalised) staged values: the
   // operator is linear, so A v - mu v = RN(1/h) (A raw - mu raw) up to
   // rounding; only the stored outputs are scaled (v itself is stored as
@@ -156,6 +164,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   const double osc = kLazy ? vrcp : 1.0;
   // j = 0 (v is v_0): <w, v_0> takes the staged input itself, no v_0 stream
   const bool v0_self = kPj && p.v0 == p.v;
+  // a lazily scaled v_0 (raw rhs, divisor *v0_scale) is scaled at use
+  const double v0rcp = (MODE == kModeIMV && p.v0_scale) ? __drcp_rn(*p.v0_scale) : 1.0;
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -247,7 +257,9 @@ __global__ void __launch_bounds__(kTmaThreads)
     }
     int Kc = (kstart == 0) ? 0 : (kstart - 1) / nu + 1;
     int posc = (kstart == 0) ? nu - 1 : (kstart - 1) - (Kc - 1) * nu;
-    int dnext = (has_drop && kstart < ke) ? p.dropped[kstart] : 0;
+    const uint8_t *dflag = p.dropped ? p.dropped : &g_no_drop;
+    const int dstep = p.dropped ? 1 : 0;
+    int dnext = (has_drop && kstart < ke) ? dflag[kstart * dstep] : 0;
     for (int i = 0; i < nsl; ++i, ++it) {
       // ---- per-slice uniform quantities
       const int k = kstart + i;
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       // (a predicated-off load still holds its scoreboard until the memory
       // pipe retires it, and shares it with the v_0 prefetch: solver
       // launches have no dropped rows and skip the load entirely)
-      if (has_drop && k + 1 < ke) dnext = p.dropped[k + 1];
+      if (has_drop && k + 1 < ke) dnext = dflag[(k + 1) * dstep];
       const int pk = (int)(((int64_t)k * m + boxx) & 1);  // row parity shifts (issue())
       const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
       const int64_t kofs = (int64_t)k * m;
@@ -376,7 +388,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (has_x) p.x_out[gi] = cur;
               if (has_out) ob[r * nx] = o;
-              const double v0r = v0_self ? vj[r] : v0v[r];
+              const double v0r = v0_self ? vj[r] : __dmul_rn(v0v[r], v0rcp);
               if (has_part) dot = FMA ? fma(o, v0r, dot) : __dadd_rn(dot, __dmul_rn(o, v0r));
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
@@ -455,7 +467,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (has_x) p.x_out[kofs + gi] = cur;
               if (has_out) p.out[kofs + gi] = o;
-              const double v0r = v0_self ? vj[r] : v0v[r];
+              const double v0r = v0_self ? vj[r] : __dmul_rn(v0v[r], v0rcp);
               if (has_part) {
                 dot = __dadd_rn(dot, __dmul_rn(o, v0r));
               }
@@ -529,6 +541,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   // normalisation of a lazily scaled basis vector: multiply by RN(1 / scale)
   // (within 1 ulp of the division; exact_scale launches take the register path)
   const double vrcp = SCALED ? __drcp_rn(*p.v_scale) : 1.0;
+  const double v0rcp = (MODE == kModeIMV && p.v0_scale) ? __drcp_rn(*p.v0_scale) : 1.0;
   double dot = 0.0;
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;
@@ -596,7 +609,9 @@ __global__ void __launch_bounds__(kTmaThreads)
     }
     int Kc = (kstart == 0) ? 0 : (kstart - 1) / nu + 1;
     int posc = (kstart == 0) ? nu - 1 : (kstart - 1) - (Kc - 1) * nu;
-    int dnext = (p.dropped && kstart < ke) ? p.dropped[kstart] : 0;
+    const uint8_t *dflag = p.dropped ? p.dropped : &g_no_drop;
+    const int dstep = p.dropped ? 1 : 0;
+    int dnext = (kstart < ke) ? dflag[kstart * dstep] : 0;
     for (int i = 0; i < nsl; ++i, ++it) {
       const int k = kstart + i;
       const bool prime = k < kb;
@@ -613,7 +628,7 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
       // dropped coupling of k: loaded one slice ahead, off the critical path
       const bool drop = dnext != 0;
-      if (p.dropped && k + 1 < ke) dnext = p.dropped[k + 1];
+      if (k + 1 < ke) dnext = dflag[(k + 1) * dstep];
       const int pk = (int)(((int64_t)k * m + boxx) & 1);  // parity of box 0
       const int pK = (int)(((int64_t)K * p.m_coarse + boxx) & 1);
       const int64_t kofs = (int64_t)k * m;
@@ -697,7 +712,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           } else {
             if (p.x_out) p.x_out[kofs + x] = cur;
             if (p.out) p.out[kofs + x] = o;
-            if (p.partials) dot = __dadd_rn(dot, __dmul_rn(o, v0v[u]));
+            if (p.partials) dot = __dadd_rn(dot, __dmul_rn(o, __dmul_rn(v0v[u], v0rcp)));
           }
         }
         qprev[u] = Qu;
@@ -829,7 +844,6 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
   } else {
     mvt = mv;
   }
-  if (mode == kModeIMV && p.v0_scale) return 0;  // lazily scaled v_0: register path
   if (p.v_scale && p.exact_scale) return 0;       // correctly rounded division
   const bool var = p.P.var || p.Q.var;
   const bool d2 = p.ny > 1;
@@ -869,7 +883,7 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       break;
     case kModeMVR:
       if (d2) {
-        if (p.fma && !var && scaled && cfg_mvr == 0 && p.v_norm_out && !p.dropped) {
+        if (p.fma && !var && scaled && cfg_mvr == 0 && !p.dropped) {
           rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                      bytes, cat);
           break;
@@ -890,10 +904,13 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       if (d2) {
         if (gather) {
           PMK_RUN(kModeIMV, 2, 4, 3, true);
-        } else if (p.fma && !var && !scaled && cfg_imv == 0 && p.out && !p.x_out && p.partials &&
-                   p.v0 && !p.dropped) {
-          rc = run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s, n_partials,
-                                                                      bytes, cat);
+        } else if (p.fma && !var && cfg_imv == 0 && p.out && !p.x_out && p.partials && p.v0 &&
+                   !p.dropped) {
+          rc = scaled ? run_tma<kModeIMV, 2, 4, 2, false, false, true, true>(p, mv, mvt, s,
+                                                                              n_partials, bytes, cat)
+                      : run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s,
+                                                                               n_partials, bytes,
+                                                                               cat);
         } else {
           switch (cfg_imv) {
             case 1: PMK_RUN(kModeIMV, 2, 4, 3, false); break;

@@ -498,15 +498,28 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
     per_iter = 8 * (lvl.total_dim + csize)
     budget = _MemoryBudget()
     budget.take(8 * lvl.total_dim)
-    w = _empty(lvl.total_dim)  # unnormalised new vector, reused every iteration
+    lazy = _lib.lazy_basis()
+    # lazy basis (pmk_lazy_basis): vs[l] holds raw basis vector l -- the rhs,
+    # then each step's w (a fresh buffer per step); otherwise the normalised
+    # v_l, with one w buffer reused every iteration
+    if lazy:
+        vs.append(b)
+    else:
+        w = _empty(lvl.total_dim)
     for j in range(max_iter):
         budget.take(per_iter)
-        v = _empty(lvl.total_dim)
         co = _empty(csize)
-        vs.append(v)
         cos.append(co)
+        if lazy:
+            v = None
+            w = _empty(lvl.total_dim)
+        else:
+            v = _empty(lvl.total_dim)
+            vs.append(v)
         _lib.check(lib.pmk_fgmres_step(H, level_idx, j, _lib.ptr(v), _lib.ptr(w), _lib.ptr(co),
                                        s), "fgmres_step")
+        if lazy:
+            vs.append(w)
         if tol is not None:
             st = _state(hier, level_idx)
             if st["breakdown"] or st["rel"] <= tol:
@@ -527,11 +540,18 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
     if st["breakdown"] or (tol is not None and n_iter and report.residual_history[-1] <= tol):
         report.converged = True
     if keep_basis:
-        basis = [vs[l].cpu().numpy() for l in range(n_iter)]
-        if not st["breakdown"]:
-            basis.append(w.cpu().numpy() / st["hraw"][n_iter, n_iter - 1])  # IEEE division
+        if lazy:  # v_l = RN(raw_l * RN(1 / scale_l)), the values the kernels use
+            scales = [st["beta"]] + [st["hraw"][l, l - 1] for l in range(1, n_iter)]
+            vn = [vs[l].reshape(-1) * (1.0 / scales[l]) for l in range(n_iter)]
+            last = vs[n_iter] if len(vs) > n_iter else None
+        else:
+            vn = vs[:n_iter]
+            last = w
+        basis = [vn[l].cpu().numpy() for l in range(n_iter)]
+        if not st["breakdown"] and last is not None:
+            basis.append(last.cpu().numpy() / st["hraw"][n_iter, n_iter - 1])  # IEEE division
         mg = isinstance(lvl.pair, MgritPair)  # cos already hold the interpolated vectors
-        pre = [(vs[l] - (cos[l] if mg else lvl.pair.interpolate(cos[l]))).cpu().numpy()
+        pre = [(vn[l] - (cos[l] if mg else lvl.pair.interpolate(cos[l]))).cpu().numpy()
                for l in range(n_iter)]
         report.metadata["basis"] = basis
         report.metadata["preconditioned"] = pre
