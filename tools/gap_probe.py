@@ -52,6 +52,10 @@ def main():
             print(f"  gaps {b:>7}: {hist[b][0]:5d}  total {hist[b][1] / 1e3:.2f} ms")
     for g, n in gaps[:12]:
         print(f"  {g:8.1f} us before {n}")
+    st = torch.cuda.memory_stats()
+    print("allocator: segments allocated", st.get("segment.all.allocated"),
+          "freed", st.get("segment.all.freed"), "alloc retries", st.get("num_alloc_retries"),
+          "device mallocs", st.get("num_device_alloc"), "frees", st.get("num_device_free"))
 
 
 if __name__ == "__main__":
