@@ -236,6 +236,16 @@ int pmk_fgmres_step(pmk_hier *H, int32_t idx, int32_t j, double *v_out,
 int32_t pmk_lazy_basis(void);
 int pmk_fgmres_finish(pmk_hier *H, int32_t idx, double *x,
                       pmk_stream_t stream);
+/* Non-blocking stop test: snapshot enqueues a copy of the level's fgmres
+ * scalars into pinned host slot `slot` (0..3) in stream order; after the
+ * caller has synchronised with that point (e.g. an event recorded right
+ * after), snapshot_read returns {beta, rel, n_iter, breakdown} as of then.
+ * Lets a driver enqueue step j+1 before it knows whether step j converged
+ * (a converged invocation turns later steps into no-ops on the device). */
+int pmk_fgmres_snapshot(pmk_hier *H, int32_t idx, int32_t slot,
+                        pmk_stream_t stream);
+int pmk_fgmres_snapshot_read(pmk_hier *H, int32_t idx, int32_t slot,
+                             double *scalars);
 /* finish restricted to the time slices [row_begin, row_end) of x (row_begin a
  * multiple of the level's coarsening factor nu); the call with row_begin = 0
  * also runs the back substitution, so it must come first.  Lets the caller

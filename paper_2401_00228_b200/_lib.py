@@ -95,6 +95,8 @@ SIGNATURES = {
     "pmk_profile_category": (ctypes.c_char_p, [c_int32]),
     "pmk_launch_count": (c_int64, []),
     "pmk_lazy_basis": (c_int32, []),
+    "pmk_fgmres_snapshot": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
+    "pmk_fgmres_snapshot_read": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "pmk_div_check": (c_int32, [c_void_p, c_double, c_int64, c_void_p, c_void_p]),
 }
 

@@ -128,6 +128,8 @@ struct LevelRT {
   std::vector<const double *> v;     // normalised basis vectors, index l
   std::vector<const double *> vt;    // child outputs, iteration j
   const int *parent_live = nullptr;
+  // pinned ring of KState snapshots (pmk_fgmres_snapshot / _read)
+  KState *snap = nullptr;
 };
 
 }  // namespace
@@ -282,7 +284,7 @@ int alloc_state(LevelRT &R, int cap) {
   const size_t n_groups = (size_t)(cap + kDotGroup - 1) / kDotGroup;
   const size_t n_dotp = n_groups * (2 * kDotGroup + 1) * kMaxPartials;
   const size_t n_doubles =
-      2 * nh + (size_t)cap * cap + 7 * (size_t)(cap + 1) + 4 * kMaxPartials + n_dotp;
+      2 * nh + (size_t)cap * cap + 8 * (size_t)(cap + 1) + 4 * kMaxPartials + n_dotp;
   const size_t bytes = sizeof(KState) + 64 + n_doubles * sizeof(double);
   PMK_CUDA_TRY(cudaMalloc(&R.d_block, bytes));
   PMK_CUDA_TRY(cudaMemset(R.d_block, 0, bytes));
@@ -308,6 +310,8 @@ int alloc_state(LevelRT &R, int cap) {
   d += cap + 1;
   h.vrcp = d;
   d += cap + 1;
+  h.hv = d;
+  d += cap + 1;
   h.lazy = lazy_basis() ? 1 : 0;
   R.partA = d;  // K-IMV <w, v_0>, then the pj block (<w, v_j>, <v_j, v_0>)
   d += 3 * kMaxPartials;
@@ -323,6 +327,8 @@ int alloc_state(LevelRT &R, int cap) {
 }
 
 inline const int *live_ptr(const LevelRT &R) { return &R.d_state->live; }
+
+constexpr int kSnapSlots = 4;
 
 int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double tol,
                  const int *parent_live, cudaStream_t s) {
@@ -792,6 +798,7 @@ void pmk_hier_destroy(pmk_hier *H) {
     for (auto &kv : R.graphs) cudaGraphExecDestroy(kv.second.first);
     if (R.d_block) cudaFree(R.d_block);
     if (R.rhs_part) cudaFree(R.rhs_part);
+    if (R.snap) cudaFreeHost(R.snap);
   }
   delete H;
 }
@@ -894,6 +901,31 @@ int pmk_fgmres_state(pmk_hier *H, int32_t idx, double *scalars, double *hist, do
     scalars[3] = (double)k.breakdown;
   }
   if (cap) *cap = R.cap;
+  return 0;
+}
+
+int pmk_fgmres_snapshot(pmk_hier *H, int32_t idx, int32_t slot, pmk_stream_t stream) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1 || slot < 0 || slot >= kSnapSlots,
+                PMK_ERR_ARG);
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.d_state, PMK_ERR_STATE);
+  if (!R.snap) PMK_CUDA_TRY(cudaHostAlloc(&R.snap, kSnapSlots * sizeof(KState), 0));
+  PMK_CUDA_TRY(cudaMemcpyAsync(R.snap + slot, R.d_state, sizeof(KState), cudaMemcpyDeviceToHost,
+                               cs(stream)));
+  return 0;
+}
+
+int pmk_fgmres_snapshot_read(pmk_hier *H, int32_t idx, int32_t slot, double *scalars) {
+  PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels - 1 || slot < 0 || slot >= kSnapSlots ||
+                    !scalars,
+                PMK_ERR_ARG);
+  LevelRT &R = H->lv[idx];
+  PMK_RETURN_IF(!R.snap, PMK_ERR_STATE);
+  const KState &k = R.snap[slot];
+  scalars[0] = k.beta;
+  scalars[1] = k.rel;
+  scalars[2] = (double)k.n_iter;
+  scalars[3] = (double)k.breakdown;
   return 0;
 }
 

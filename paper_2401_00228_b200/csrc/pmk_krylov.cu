@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(1024)
     if (lane == 0) {
       c[i] = hi;
       h[(int64_t)i * ld + j] = hi;
+      st->hv[i] = __dmul_rn(hi, st->vrcp[i]);  // update coefficient (lazy: h_i / scale_i)
     }
     __syncwarp();
   }
@@ -438,8 +439,8 @@ __global__ void __launch_bounds__(kRedThreads)
   double hq[CNT];
   const double2 *c2[CNT];
 #pragma unroll
-  for (int q = 0; q < CNT; ++q) {  // (lazy basis: h_q v_q = (h_q vrcp_q) raw_q)
-    hq[q] = __dmul_rn(st->h[(int64_t)(i0 + q) * ld + j], st->vrcp[i0 + q]);
+  for (int q = 0; q < CNT; ++q) {  // h_q (x vrcp_q for a lazy basis), icwy_solve
+    hq[q] = st->hv[i0 + q];
     c2[q] = reinterpret_cast<const double2 *>(V.v[q]);
   }
   double acc[1] = {0.0};
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(kRedThreads)
   double hq[kGroup];
 #pragma unroll
   for (int q = 0; q < kGroup; ++q)
-    hq[q] = (q < count) ? __dmul_rn(st->h[(int64_t)(i0 + q) * ld + j], st->vrcp[i0 + q]) : 0.0;
+    hq[q] = (q < count) ? st->hv[i0 + q] : 0.0;
   double acc[1] = {0.0};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
@@ -577,6 +578,12 @@ __global__ void __launch_bounds__(256)
   const int n_iter = st->n_iter;
   const int hi = min(n_iter, first + a.count);
   if (first > 0 && first >= n_iter) return;
+  __shared__ double ys[kAsmChunk], sc[kAsmChunk];  // y_l and the lazy-basis scales
+  for (int q = threadIdx.x; q < kAsmChunk; q += blockDim.x) {
+    ys[q] = (first + q < hi) ? st->y[first + q] : 0.0;
+    sc[q] = (first + q < hi) ? st->vrcp[first + q] : 1.0;
+  }
+  __syncthreads();
   for (int k = blockIdx.y; k < rows; k += gridDim.y) {
     const int K = (k == 0) ? 0 : (k - 1) / nu + 1;
     const int64_t base = (int64_t)k * m;
@@ -587,9 +594,9 @@ __global__ void __launch_bounds__(256)
       double acc = (first == 0) ? 0.0 : x[e];
       for (int l = first; l < hi; ++l) {
         const int q = l - first;
-        const double vl = __dmul_rn(__ldg(a.v[q] + e), st->vrcp[l]);  // (lazy basis)
+        const double vl = __dmul_rn(__ldg(a.v[q] + e), sc[q]);  // (lazy basis)
         const double xl = __dsub_rn(vl, __ldg(a.vt[q] + ci));
-        acc = __dadd_rn(acc, __dmul_rn(st->y[l], xl));
+        acc = __dadd_rn(acc, __dmul_rn(ys[q], xl));
       }
       x[e] = acc;
     }

@@ -19,6 +19,7 @@ struct KState {
   // vrcp[l] = RN(1 / vscale[l]) -- the exact values an explicit normalisation
   // pass would have stored.  lazy = 0: stored normalised, vrcp[l] = 1.
   double *vrcp;
+  double *hv;  // current column's update coefficients h_i * vrcp_i (ICWY)
   int lazy;
   double *hist;    // residual history rel_j
   double *gram;    // cap x cap, row i = <v_i, v_l>, l < i (ICWY MGS)

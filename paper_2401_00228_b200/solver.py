@@ -506,6 +506,12 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
         vs.append(b)
     else:
         w = _empty(lvl.total_dim)
+    # Stop test one step behind: step j is enqueued before the host looks at
+    # the snapshot taken after step j-1 (pmk_fgmres_snapshot), so the GPU
+    # never idles on the host round trip; once an iteration has converged the
+    # device turns the already enqueued next step into no-ops.
+    snaps = {}
+    sc = (ctypes.c_double * 4)()
     for j in range(max_iter):
         budget.take(per_iter)
         co = _empty(csize)
@@ -521,9 +527,16 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
         if lazy:
             vs.append(w)
         if tol is not None:
-            st = _state(hier, level_idx)
-            if st["breakdown"] or st["rel"] <= tol:
-                break
+            _lib.check(lib.pmk_fgmres_snapshot(H, level_idx, j % 4, s), "snapshot")
+            ev = torch.cuda.Event()
+            ev.record()
+            snaps[j] = ev
+            if j >= 1:
+                snaps.pop(j - 1).synchronize()
+                _lib.check(lib.pmk_fgmres_snapshot_read(H, level_idx, (j - 1) % 4, sc),
+                           "snapshot_read")
+                if sc[3] or sc[1] <= tol:  # breakdown / converged at step j-1
+                    break
     x = _empty(lvl.total_dim)
     if copier is None:
         _lib.check(lib.pmk_fgmres_finish(H, level_idx, _lib.ptr(x), s), "fgmres_finish")
