@@ -550,12 +550,18 @@ int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cuda
   const int64_t coff = (int64_t)(row0 / nu) * (R.P.mgrit ? m : R.P.m_coarse);
   const int64_t n_sub = (int64_t)(row1 - row0) * m;
   const int n = (int)R.vt.size();
+  // time pairs with nu = 2 take the pair kernel (<= 8 vectors per pass, every
+  // coarse value read once, all loads up front); more vectors are summed in
+  // passes of 8 -- two extra x read/write sweeps for 19 vectors still beat
+  // the one-pass generic kernel's dependent per-element loop (4.4 TB/s)
+  const bool pair = !R.P.mgrit && !R.P.group_of && R.P.nu == 2 && R.P.m_coarse == m;
+  const int per_pass = pair ? 8 : kAsmChunk;
   int first = 0;
   do {
     AssembleArgs a;
     std::memset(&a, 0, sizeof(a));
     a.count = 0;
-    for (int l = first; l < n && a.count < kAsmChunk; ++l) {
+    for (int l = first; l < n && a.count < per_pass; ++l) {
       a.v[a.count] = R.v[l] + off;
       a.vt[a.count] = R.vt[l] + coff;
       ++a.count;
@@ -566,7 +572,7 @@ int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cuda
       rc = launch_assemble(R.d_state, a, x + off, n_sub, m, R.P.nu, R.P.m_coarse,
                            R.P.group_of, first, s);
     if (rc) return rc;
-    first += kAsmChunk;
+    first += per_pass;
   } while (first < n);
   return 0;
 }

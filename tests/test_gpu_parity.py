@@ -241,6 +241,39 @@ def test_host_output_slabs_bitwise(name):
         assert ro.outer_iterations == rd.outer_iterations
 
 
+@pytest.mark.parametrize("name", ["c5_small", "c4_small", "mgrit2_small", "c2_small"])
+def test_lazy_basis_matches_normalised_basis(name):
+    """The lazy Krylov basis (default) against the explicitly normalised one
+    (PMK_LAZY=0, run in a subprocess: the mode is fixed per process): same
+    iterations, x within 1e-12 (only where the scales are folded -- dot
+    products, update coefficients -- does the rounding differ)."""
+    import json
+    import subprocess
+    import sys
+    import tempfile
+
+    from paper_2401_00228_b200 import _lib, multilevel_solve
+
+    assert _lib.lazy_basis()
+    case = SMALL[name]
+    x, rep = multilevel_solve(gpu_hierarchy(case))
+    code = ("import json,sys; sys.path.insert(0, %r); import numpy as np; "
+            "from tests.cases import SMALL, gpu_hierarchy; "
+            "from paper_2401_00228_b200 import _lib, multilevel_solve; "
+            "assert not _lib.lazy_basis(); "
+            "x, r = multilevel_solve(gpu_hierarchy(SMALL[%r])); "
+            "np.save(sys.argv[1], x); print(json.dumps(r.outer_iterations))"
+            % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), name))
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "x.npy")
+        env = dict(os.environ, PMK_LAZY="0")
+        out = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True,
+                             text=True, check=True)
+        xn = np.load(path)
+    assert json.loads(out.stdout.strip().splitlines()[-1]) == rep.outer_iterations
+    assert rel(x, xn) <= 1e-12, rel(x, xn)
+
+
 def test_sequential_solve_matches_oracle():
     from oracle import pintmk_oracle as O
     from paper_2401_00228_b200 import (ThetaSchemeConfig, build_laplacian,
