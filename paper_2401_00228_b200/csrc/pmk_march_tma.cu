@@ -884,18 +884,20 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
     case kModeMVR:
       if (d2) {
         if (p.fma && !var && scaled && !p.dropped && (cfg_mvr == 0 || cfg_mvr >= 4)) {
-          // in-solver K-MVR; tuning variants (PMK_TMA_CFG=4/5/6,x): 8x2, 8x3, 4x4
+          // in-solver K-MVR: 8-row tiles x 3 stages (no pre-pass since the lazy
+          // basis, so the taller tile's per-slice savings win over occupancy:
+          // -3% vs 4x3 by ncu, tools/march_ab_env.sh); PMK_TMA_CFG=4/6,x: 8x2, 4x4
           if (cfg_mvr == 4)
             rc = run_tma<kModeMVR, 2, 8, 2, false, false, true, true>(p, mv, mvt, s, n_partials,
-                                                                       bytes, cat);
-          else if (cfg_mvr == 5)
-            rc = run_tma<kModeMVR, 2, 8, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat);
           else if (cfg_mvr == 6)
             rc = run_tma<kModeMVR, 2, 4, 4, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat);
-          else
+          else if (cfg_mvr == 7)
             rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
+                                                                       bytes, cat);
+          else
+            rc = run_tma<kModeMVR, 2, 8, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat);
           break;
         }
