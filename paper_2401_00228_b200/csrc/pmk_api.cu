@@ -498,10 +498,12 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412);
     // the last step of a fixed-budget inner solve needs only ||w||, not w
     int n_norm = 0;
+    bool finished = false;  // (finish_col fused into the last update pass)
     rc = launch_icwy_mgs(R.d_state, R.cap, j, w_next, R.v.data(), R.N, R.partA, np,
-                         pj_done ? pj : nullptr, R.partM, R.partB, &n_norm, keep_w, s);
+                         pj_done ? pj : nullptr, R.partM, R.partB, &n_norm, keep_w, s, R.tol,
+                         true, &finished);
     if (rc) return rc;
-    rc = launch_finish_col(R.d_state, R.cap, j, R.partB, n_norm, R.tol, s);
+    if (!finished) rc = launch_finish_col(R.d_state, R.cap, j, R.partB, n_norm, R.tol, s);
     if (rc) return rc;
     R.pending = w_next;
     R.vt.push_back(child_out);

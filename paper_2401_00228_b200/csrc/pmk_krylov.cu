@@ -428,12 +428,65 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// h[j+1][j] = ||w||, breakdown test, Givens update (solver.py:412-440), by
+// one block (all its threads take part in the reduction).
+__device__ __forceinline__ void finish_col_block(KState *st, int ld, int j,
+                                                 const double *partials, int n_partials,
+                                                 double tol) {
+  const double ss = reduce_partials(partials, n_partials);
+  if (threadIdx.x != 0) return;
+  double *h = st->h;
+  const double hn = sqrt(ss);
+  h[(j + 1) * ld + j] = hn;
+  for (int l = 0; l <= j + 1; ++l) st->hraw[l * ld + j] = h[l * ld + j];
+  st->n_iter = j + 1;
+  double cn2 = 0.0;  // np.linalg.norm(h[:j+2, j])
+  for (int l = 0; l <= j + 1; ++l) cn2 = __dadd_rn(cn2, __dmul_rn(h[l * ld + j], h[l * ld + j]));
+  const double col_norm = sqrt(cn2);
+  const bool breakdown = hn <= 1e-14 * fmax(col_norm, 1e-300);
+  if (!breakdown) {
+    st->vscale[j + 1] = hn;
+    st->vrcp[j + 1] = st->lazy ? __drcp_rn(hn) : 1.0;
+  }
+  double *cs = st->cs, *sn = st->sn, *g = st->g;
+  for (int l = 0; l < j; ++l) {
+    const double a = h[l * ld + j], b = h[(l + 1) * ld + j];
+    const double tmp = __dadd_rn(__dmul_rn(cs[l], a), __dmul_rn(sn[l], b));
+    h[(l + 1) * ld + j] = __dadd_rn(__dmul_rn(-sn[l], a), __dmul_rn(cs[l], b));
+    h[l * ld + j] = tmp;
+  }
+  const double hjj = h[j * ld + j], hj1 = h[(j + 1) * ld + j];
+  const double denom = hypot(hjj, hj1);
+  cs[j] = __ddiv_rn(hjj, denom);
+  sn[j] = __ddiv_rn(hj1, denom);
+  h[j * ld + j] = denom;
+  h[(j + 1) * ld + j] = 0.0;
+  g[j + 1] = __dmul_rn(-sn[j], g[j]);
+  g[j] = __dmul_rn(cs[j], g[j]);
+  const double rel = __ddiv_rn(fabs(g[j + 1]), st->beta);
+  st->rel = rel;
+  st->hist[j] = rel;
+  if (breakdown) {
+    st->breakdown = 1;
+    st->live = 0;
+  } else if (tol > 0.0 && rel <= tol) {
+    st->live = 0;  // converged (solver.py:438-440)
+  }
+}
+
+__global__ void finish_col_kernel(KState *st, int ld, int j, const double *partials,
+                                  int n_partials, double tol) {
+  if (!st->live) return;
+  finish_col_block(st, ld, j, partials, n_partials, tol);
+}
+
 // w -= sum_q h[i0+q][j] v_q (ascending q, the reference's per-element
 // rounding); with `partials`, the partial sums of ||w||^2 of the result.
 template <int CNT>
 __global__ void __launch_bounds__(kRedThreads)
-    icwy_update_vec_kernel(const KState *st, int ld, int j, int i0, MultiVec V,
-                           double *__restrict__ w, int64_t n, double *partials, bool store) {
+    icwy_update_vec_kernel(KState *st, int ld, int j, int i0, MultiVec V,
+                           double *__restrict__ w, int64_t n, double *partials, bool store,
+                           bool finish, double tol) {
   if (!st->live) return;
   constexpr int U = (12 / (CNT + 1)) > 1 ? 12 / (CNT + 1) : 1;
   double hq[CNT];
@@ -487,6 +540,18 @@ __global__ void __launch_bounds__(kRedThreads)
     if (partials) acc[0] = __dadd_rn(acc[0], __dmul_rn(a, a));
   }
   if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
+  if (finish) {  // last block to finish runs finish_col (fixed-order reduction)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      finish_col_block(st, ld, j, partials, gridDim.x, tol);
+      if (threadIdx.x == 0) st->ticket = 0;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kRedThreads)
@@ -510,50 +575,6 @@ __global__ void __launch_bounds__(kRedThreads)
   if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
 }
 
-// h[j+1][j] = ||w||, breakdown test, Givens update (solver.py:412-440).
-__global__ void finish_col_kernel(KState *st, int ld, int j, const double *partials,
-                                  int n_partials, double tol) {
-  if (!st->live) return;
-  const double ss = reduce_partials(partials, n_partials);
-  if (threadIdx.x != 0) return;
-  double *h = st->h;
-  const double hn = sqrt(ss);
-  h[(j + 1) * ld + j] = hn;
-  for (int l = 0; l <= j + 1; ++l) st->hraw[l * ld + j] = h[l * ld + j];
-  st->n_iter = j + 1;
-  double cn2 = 0.0;  // np.linalg.norm(h[:j+2, j])
-  for (int l = 0; l <= j + 1; ++l) cn2 = __dadd_rn(cn2, __dmul_rn(h[l * ld + j], h[l * ld + j]));
-  const double col_norm = sqrt(cn2);
-  const bool breakdown = hn <= 1e-14 * fmax(col_norm, 1e-300);
-  if (!breakdown) {
-    st->vscale[j + 1] = hn;
-    st->vrcp[j + 1] = st->lazy ? __drcp_rn(hn) : 1.0;
-  }
-  double *cs = st->cs, *sn = st->sn, *g = st->g;
-  for (int l = 0; l < j; ++l) {
-    const double a = h[l * ld + j], b = h[(l + 1) * ld + j];
-    const double tmp = __dadd_rn(__dmul_rn(cs[l], a), __dmul_rn(sn[l], b));
-    h[(l + 1) * ld + j] = __dadd_rn(__dmul_rn(-sn[l], a), __dmul_rn(cs[l], b));
-    h[l * ld + j] = tmp;
-  }
-  const double hjj = h[j * ld + j], hj1 = h[(j + 1) * ld + j];
-  const double denom = hypot(hjj, hj1);
-  cs[j] = __ddiv_rn(hjj, denom);
-  sn[j] = __ddiv_rn(hj1, denom);
-  h[j * ld + j] = denom;
-  h[(j + 1) * ld + j] = 0.0;
-  g[j + 1] = __dmul_rn(-sn[j], g[j]);
-  g[j] = __dmul_rn(cs[j], g[j]);
-  const double rel = __ddiv_rn(fabs(g[j + 1]), st->beta);
-  st->rel = rel;
-  st->hist[j] = rel;
-  if (breakdown) {
-    st->breakdown = 1;
-    st->live = 0;
-  } else if (tol > 0.0 && rel <= tol) {
-    st->live = 0;  // converged (solver.py:438-440)
-  }
-}
 
 // Back substitution (solver.py:442-444).
 __global__ void backsolve_kernel(KState *st, int ld) {
@@ -793,10 +814,10 @@ void dots_vec(const KState *st, const double *w, const double *vj, const MultiVe
   icwy_dots_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, w, vj, V, n, partials);
 }
 template <int CNT>
-void update_vec(const KState *st, int ld, int j, int i0, const MultiVec &V, double *w, int64_t n,
-                double *partials, bool store, cudaStream_t s) {
+void update_vec(KState *st, int ld, int j, int i0, const MultiVec &V, double *w, int64_t n,
+                double *partials, bool store, bool finish, double tol, cudaStream_t s) {
   icwy_update_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, w, n,
-                                                                 partials, store);
+                                                                 partials, store, finish, tol);
 }
 
 #define PMK_CASES8(F) F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8)
@@ -807,7 +828,9 @@ void update_vec(const KState *st, int ld, int j, int i0, const MultiVec &V, doub
 // passes use the fixed kRedBlocks grid (deterministic partial layout).
 int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
                     const double *c0p, int n_c0, const double *pj, double *dot_partials,
-                    double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s) {
+                    double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s, double tol,
+                    bool fuse_finish, bool *finished) {
+  if (finished) *finished = false;
   auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   bool vec = al(w);
   for (int i = 0; i <= j; ++i) vec = vec && al(v[i]);
@@ -850,6 +873,8 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
     MultiVec V{};
     for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
     const bool store = keep_w || !last;
+    const bool fin = last && fuse_finish && vec;
+    if (fin && finished) *finished = true;
     prof::Scope scope(prof::kMGS, 8.0 * (cnt + (store ? 2 : 1)) * (double)n,
                       2.0 * (cnt + (last ? 1 : 0)) * (double)n, s);
     double *part = last ? norm_partials : nullptr;
@@ -857,7 +882,7 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
       switch (cnt) {
 #define PMK_UPD_CASE(C)                                \
   case C:                                              \
-    update_vec<C>(st, ld, j, i0, V, w, n, part, store, s); \
+    update_vec<C>(st, ld, j, i0, V, w, n, part, store, fin, tol, s); \
     break;
         PMK_CASES16(PMK_UPD_CASE)
 #undef PMK_UPD_CASE

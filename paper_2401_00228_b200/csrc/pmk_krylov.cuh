@@ -21,6 +21,7 @@ struct KState {
   double *vrcp;
   double *hv;  // current column's update coefficients h_i * vrcp_i (ICWY)
   int lazy;
+  unsigned int ticket;  // blocks done in a pass that ends with a fused finish
   double *hist;    // residual history rel_j
   double *gram;    // cap x cap, row i = <v_i, v_l>, l < i (ICWY MGS)
   double beta, rel;
@@ -44,9 +45,13 @@ struct MultiVec {
   const double *v[kGroup];
 };
 // dot partial buffer: ceil(cap / kDotGroup) * (2 kDotGroup + 1) * kMaxPartials doubles
+// With fuse_finish (and aligned operands) the last block of the last update
+// pass also runs finish_col (h[j+1][j], Givens, stop test); *finished tells
+// the caller whether it still has to launch it.
 int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
                     const double *c0p, int n_c0, const double *pj, double *dot_partials,
-                    double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s);
+                    double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s,
+                    double tol = 0.0, bool fuse_finish = false, bool *finished = nullptr);
 
 int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
                  cudaStream_t s);
