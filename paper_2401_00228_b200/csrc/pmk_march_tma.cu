@@ -165,7 +165,9 @@ __global__ void __launch_bounds__(kTmaThreads)
   // j = 0 (v is v_0): <w, v_0> takes the staged input itself, no v_0 stream
   const bool v0_self = kPj && p.v0 == p.v;
   // a lazily scaled v_0 (raw rhs, divisor *v0_scale) is scaled at use
-  const double v0rcp = (MODE == kModeIMV && p.v0_scale) ? __drcp_rn(*p.v0_scale) : 1.0;
+  // a lazily scaled v_0 (raw rhs, divisor *v0_scale): the dot products with
+  // it are accumulated raw and scaled once at the end (j >= 1; at j = 0 the
+  // staged, already scaled input is v_0 itself)
   double vsq = 0.0;  // K-MVR: partial ||vh||^2 of the values this thread stores
   uint32_t it = 0;  // slices consumed by this CTA (ring position)
 
@@ -388,7 +390,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (has_x) p.x_out[gi] = cur;
               if (has_out) ob[r * nx] = o;
-              const double v0r = v0_self ? vj[r] : __dmul_rn(v0v[r], v0rcp);
+              const double v0r = v0_self ? vj[r] : v0v[r];
               if (has_part) dot = FMA ? fma(o, v0r, dot) : __dadd_rn(dot, __dmul_rn(o, v0r));
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(kTmaThreads)
             } else {
               if (has_x) p.x_out[kofs + gi] = cur;
               if (has_out) p.out[kofs + gi] = o;
-              const double v0r = v0_self ? vj[r] : __dmul_rn(v0v[r], v0rcp);
+              const double v0r = v0_self ? vj[r] : v0v[r];
               if (has_part) {
                 dot = __dadd_rn(dot, __dmul_rn(o, v0r));
               }
@@ -488,6 +490,11 @@ __global__ void __launch_bounds__(kTmaThreads)
         issue(k + S, stage);
       }
     }
+  }
+  if (MODE == kModeIMV && p.v0_scale && !v0_self) {
+    const double v0rcp = __drcp_rn(*p.v0_scale);
+    dot = __dmul_rn(dot, v0rcp);
+    dgj = __dmul_rn(dgj, v0rcp);
   }
   if (MODE == kModeIMV && has_part) {
     const double s = block_sum(dot);
