@@ -252,7 +252,9 @@ def run_ours(args):
         del h2, xh
         gc.collect()  # the previous hierarchy's native teardown (cudaFree
         # synchronises) happens here, not inside the next timed step
-    e2e_s = pdist.max_over_ranks(max(e2e_t), device="cuda") if e2e_t else float("nan")
+    # per-step mean (total time / steps, like the device-timed value), max over ranks
+    e2e_s = (pdist.max_over_ranks(sum(e2e_t) / len(e2e_t), device="cuda") if e2e_t
+             else float("nan"))
 
     # ----- roofline of the dominant memory-bound kernel
     peak, peak_kind = peaks()
