@@ -219,13 +219,27 @@ bool lazy_basis() {
   return on;
 }
 
+// Deferred first orthogonalisation in fixed-budget inner solves (PMK_FUSE01=0
+// turns it off): see fgmres_fixed.
+bool fuse01() {
+  static const bool on = [] {
+    const char *e = getenv("PMK_FUSE01");
+    return lazy_basis() && !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // vh = Y^T (A v - mu v) ; optionally v_norm_out = v (normalised input)
 int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
            const double *v_scale, double *vh, double *scratch, double *v_norm_out,
            const int *live, cudaStream_t s, bool exact = true, double *vh_partials = nullptr,
-           int *n_vh = nullptr) {
+           int *n_vh = nullptr, const double *v_sub = nullptr,
+           const double *v_sub_coef = nullptr, double *vn_partials = nullptr) {
   MarchParams p = base_params(L);
   p.v = v;
+  p.v_sub = v_sub;
+  p.v_sub_coef = v_sub_coef;
+  p.vn_partials = vn_partials;
   p.v_scale = v_scale;
   p.v_norm_out = v_norm_out;
   p.mu = mu;
@@ -240,7 +254,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   p.vh_partials = space ? nullptr : vh_partials;  // a space pair gathers afterwards
   int np = 0;
   int rc = launch_march(kModeMVR, p, s, &np);
-  if (n_vh) *n_vh = p.vh_partials ? np : 0;
+  if (n_vh) *n_vh = (p.vh_partials || p.vn_partials) ? np : 0;
   if (rc) return rc;
   if (space) {
     prof::Tag tag(t_level, prof::kHintRestrict);
@@ -357,7 +371,8 @@ int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double t
   return 0;
 }
 
-int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s);
+int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s,
+                 const double *out_scale = nullptr);
 
 bool graphs_enabled() {
   static const bool on = [] {
@@ -372,11 +387,12 @@ bool graphs_enabled() {
 // so it is captured once per output buffer into a CUDA graph and replayed
 // (the first call runs eagerly so that lazy one-time initialisation -- kernel
 // attributes, constant tables -- never happens inside a capture).
-int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cudaStream_t s) {
+int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cudaStream_t s,
+                       const double *out_scale = nullptr) {
   LevelRT &R = H->lv[child];
   if (!graphs_enabled() || R.graph_failed || s == nullptr || s == cudaStreamLegacy ||
       s == cudaStreamPerThread)
-    return fgmres_fixed(H, child, out, live, s);
+    return fgmres_fixed(H, child, out, live, s, out_scale);
   auto it = R.graphs.find(out);
   if (it != R.graphs.end()) {
     g_launches.fetch_add(it->second.second);  // the graph's kernel nodes
@@ -385,15 +401,15 @@ int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cud
   }
   if (!R.seen.count(out)) {
     R.seen.insert(out);
-    return fgmres_fixed(H, child, out, live, s);
+    return fgmres_fixed(H, child, out, live, s, out_scale);
   }
   const int64_t before = g_launches.load();
   if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     cudaGetLastError();
     R.graph_failed = true;
-    return fgmres_fixed(H, child, out, live, s);
+    return fgmres_fixed(H, child, out, live, s, out_scale);
   }
-  int rc = fgmres_fixed(H, child, out, live, s);
+  int rc = fgmres_fixed(H, child, out, live, s, out_scale);
   cudaGraph_t g = nullptr;
   cudaError_t e = cudaStreamEndCapture(s, &g);
   const int64_t nodes = g_launches.load() - before;
@@ -411,19 +427,32 @@ int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cud
   cudaGetLastError();
   R.graph_failed = true;
   if (rc) return rc;
-  return fgmres_fixed(H, child, out, live, s);
+  return fgmres_fixed(H, child, out, live, s, out_scale);
 }
 
-// Child solve of level idx: vt = A_{idx+1}^{-1} vh (approximately).
-int child_solve(pmk_hier *H, int idx, double *out, const int *live, cudaStream_t s) {
+// Child solve of level idx: vt = A_{idx+1}^{-1} vh (approximately); with
+// out_scale, the solution for vh * (*out_scale) (every child solve is
+// homogeneous in its rhs: the FGMRES iterates scale with it).
+int child_solve(pmk_hier *H, int idx, double *out, const int *live, cudaStream_t s,
+                const double *out_scale = nullptr) {
   const int child = idx + 1;
   if (child == H->n_levels - 1) {
     PMK_RETURN_IF(!H->has_coarse || !H->coarse_rhs, PMK_ERR_STATE);
     prof::Tag tag(child);
-    return coarse_solve(H->coarse, H->coarse_rhs, out, live, s);
+    return coarse_solve(H->coarse, H->coarse_rhs, out, live, s, out_scale);
   }
-  if (idx == 0) return fgmres_fixed_graph(H, child, out, live, s);
-  return fgmres_fixed(H, child, out, live, s);
+  if (idx == 0) return fgmres_fixed_graph(H, child, out, live, s, out_scale);
+  return fgmres_fixed(H, child, out, live, s, out_scale);
+}
+
+// Can child_solve(idx) honour an out_scale?
+bool child_scalable(const pmk_hier *H, int idx) {
+  const int child = idx + 1;
+  if (child == H->n_levels - 1) {
+    const pmk_coarse &C = H->coarse;
+    return H->has_coarse && C.kind == PMK_COARSE_DST && C.fft_x && C.dim == 2 && C.ny > 1;
+  }
+  return true;
 }
 
 double *child_rhs(pmk_hier *H, int idx) {
@@ -447,8 +476,14 @@ int mvr_into_child(pmk_hier *H, int idx, const double *v, const double *v_scale,
   return rc;
 }
 
+// fuse (fgmres_fixed only): kStepDefer = step 0 stops after h_00 (its w stays
+// unorthogonalised in w_next); kStepSub = step 1 starts with the deferred
+// update, fused into its K-MVR, which stores v_1 raw into sub_store.
+constexpr int kStepPlain = 0, kStepDefer = 1, kStepSub = 2;
+
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
-                cudaStream_t s, bool keep_w = true) {
+                cudaStream_t s, bool keep_w = true, int fuse = kStepPlain,
+                double *sub_store = nullptr) {
   prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
@@ -468,9 +503,30 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
   // the reference's division).  Normalised basis: this pass also stores v_j
   // into v_out.  Lazy basis: v_j stays raw (every consumer scales it); v_out,
   // if given, still receives the normalised copy.
-  int rc = mvr_into_child(H, idx, R.pending, K.vscale + j, v_out, live, s, classic_mgs());
-  if (rc) return rc;
-  R.v.push_back(lazy ? R.pending : v_out);
+  int rc;
+  const double *child_scale = nullptr;
+  if (fuse == kStepSub) {
+    // deferred step-0 update fused into this K-MVR: it stages w_0 and v_0,
+    // forms v_1 raw = w_0 - h_00 v_0 (update-pass rounding), stores it, and
+    // restricts (A - mu) v_1 raw; then finish_col(0) gives h_10 from the
+    // stored values.  The child solve is homogeneous, so it is asked for the
+    // solution of (its rhs) / h_10 directly (out_scale = RN(1/h_10)).
+    LevelRT *C = (idx + 1 < H->n_levels - 1) ? &H->lv[idx + 1] : nullptr;
+    double *part = (C && C->rhs_part) ? C->rhs_part : nullptr;
+    int n = 0;
+    rc = do_mvr(R.L, R.P, H->mu, R.pending, nullptr, child_rhs(H, idx), R.ts_scratch, sub_store,
+                live, s, false, part, &n, R.v[0], K.hv, R.partB);
+    if (rc) return rc;
+    if (C) C->rhs_part_n = part ? n : 0;
+    rc = launch_finish_col(R.d_state, R.cap, 0, R.partB, n, R.tol, s);
+    if (rc) return rc;
+    R.v.push_back(sub_store);
+    child_scale = K.vrcp + 1;
+  } else {
+    rc = mvr_into_child(H, idx, R.pending, K.vscale + j, v_out, live, s, classic_mgs());
+    if (rc) return rc;
+    R.v.push_back(lazy ? R.pending : v_out);
+  }
   if (R.P.mgrit) {
     // coarse solve into the pair's scratch, then ideal interpolation into the
     // iteration's (fine-size) child_out (intergrid.py:157-167)
@@ -479,7 +535,7 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     prof::Tag tag(idx, prof::kHintInterp);
     rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, live, s);
   } else {
-    rc = child_solve(H, idx, child_out, live, s);
+    rc = child_solve(H, idx, child_out, live, s, child_scale);
   }
   if (rc) return rc;
   // w = A (v_j - Z vt) and partial <w, v_0>   (solver.py:359, 403, 407);
@@ -494,6 +550,13 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
               R.v[0], lazy ? K.vscale : nullptr, R.partA, &np, live, s, !classic_mgs(), pj,
               &pj_done);
   if (rc) return rc;
+  if (fuse == kStepDefer) {  // h_00 only; update + finish_col(0) follow in step 1
+    rc = launch_icwy_solve(R.d_state, R.cap, 0, R.partA, np, s);
+    if (rc) return rc;
+    R.pending = w_next;
+    R.vt.push_back(child_out);
+    return 0;
+  }
   if (!classic_mgs()) {
     // MGS (solver.py:405-408) in its one-reduce form, ||w|| (solver.py:412);
     // the last step of a fixed-budget inner solve needs only ||w||, not w
@@ -534,7 +597,8 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
 // coarse slice J, so the sub-range starting there is itself a (shorter)
 // space-time vector whose slice 0 maps to coarse slice J, exactly the
 // assembly's slice mapping -- it runs on offset views.
-int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cudaStream_t s) {
+int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cudaStream_t s,
+                       const double *out_scale = nullptr) {
   prof::Tag tag(idx);
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
@@ -545,7 +609,7 @@ int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cuda
   PMK_RETURN_IF(row0 < 0 || row1 > rows || row0 >= row1 || row0 % nu != 0, PMK_ERR_ARG);
   int rc = 0;
   if (row0 == 0) {
-    rc = launch_backsolve(R.d_state, R.cap, s);
+    rc = launch_backsolve(R.d_state, R.cap, s, out_scale);
     if (rc) return rc;
   }
   const int64_t off = (int64_t)row0 * m;
@@ -579,13 +643,15 @@ int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cuda
   return 0;
 }
 
-int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s) {
+int fgmres_finish(pmk_hier *H, int idx, double *x, cudaStream_t s,
+                  const double *out_scale = nullptr) {
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.d_state, PMK_ERR_STATE);
-  return fgmres_finish_rows(H, idx, x, 0, (int)(R.N / R.P.m_fine), s);
+  return fgmres_finish_rows(H, idx, x, 0, (int)(R.N / R.P.m_fine), s, out_scale);
 }
 
-int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s) {
+int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaStream_t s,
+                 const double *out_scale) {
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set || !R.rhs, PMK_ERR_STATE);
   PMK_RETURN_IF((int)R.v_slots.size() < R.budget || (int)R.child_out.size() < R.budget ||
@@ -594,15 +660,31 @@ int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaSt
   int rc = fgmres_begin(H, idx, R.rhs, R.budget, 0.0, parent_live, s);
   if (rc) return rc;
   const bool lazy = R.h_state.lazy != 0;
+  // Deferred first orthogonalisation: step 0's update pass (w_0 -= h_00 v_0,
+  // 24 B per unknown) is fused into step 1's K-MVR, which reads w_0 and v_0
+  // anyway-adjacent (+8 B): 2-D constant-stencil time pairs, lazy basis.
+  const bool fuse = fuse01() && lazy && R.budget >= 2 && !R.P.mgrit && !R.P.group_of &&
+                    R.L.dim == 2 && !R.L.diag_t.var && !R.L.sub_t.var && !R.L.dropped &&
+                    child_scalable(H, idx);
   for (int j = 0; j < R.budget; ++j) {
     // lazy basis: v_0 is the rhs, step j's w goes to slot j+1 (it is basis
     // vector j+1), the last step's w only feeds ||w|| (w_buf)
     double *w_next = (lazy && j + 1 < R.budget) ? R.v_slots[j + 1] : R.w_buf;
+    int mode = kStepPlain;
+    double *store = nullptr;
+    if (fuse && j == 0) {
+      mode = kStepDefer;
+      w_next = R.w_buf;  // w_0 raw, consumed by step 1's K-MVR
+    } else if (fuse && j == 1) {
+      mode = kStepSub;
+      store = R.v_slots[1];  // v_1 raw
+      w_next = (2 < R.budget) ? R.v_slots[2] : R.w_buf;
+    }
     rc = fgmres_step(H, idx, j, lazy ? nullptr : R.v_slots[j], w_next, R.child_out[j], s,
-                     j + 1 < R.budget);
+                     j + 1 < R.budget, mode, store);
     if (rc) return rc;
   }
-  return fgmres_finish(H, idx, x, s);
+  return fgmres_finish(H, idx, x, s, out_scale);
 }
 
 // Internal scratch for the stand-alone reductions.

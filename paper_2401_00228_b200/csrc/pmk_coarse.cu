@@ -121,10 +121,11 @@ constexpr int kRecBatch = 8;
 __global__ void __launch_bounds__(256)
     dst_recurrence_kernel(double *X, const double *delta, const double *beta,
                           const uint8_t *dropped, int n_steps, int m, double scale,
-                          const int *live) {
+                          const int *live, const double *out_scale = nullptr) {
   if (!is_live(live)) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
+  if (out_scale) scale *= *out_scale;  // (the solve is linear in the rhs)
   // multiply by 1/delta: high modes decay through the subnormal range, where
   // an IEEE division takes the slow path
   const double d = 1.0 / delta[i], b = beta[i];
@@ -226,10 +227,12 @@ int run_recurrence(const pmk_coarse &C, double *X, int m, double scale, double *
   return 0;
 }
 
-__global__ void copy_row_kernel(const double *src, double *dst, int m, const int *live) {
+__global__ void copy_row_kernel(const double *src, double *dst, int m, const int *live,
+                                const double *scale = nullptr) {
   if (!is_live(live)) return;
+  const double c = scale ? *scale : 1.0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
-    dst[i] = src[i];
+    dst[i] = scale ? __dmul_rn(src[i], c) : src[i];
 }
 
 // b = rhs_k + [k not dropped] * C out_{k-1}  (row-form 5-slot stencil)
@@ -390,11 +393,13 @@ int mgrit_interpolate(const pmk_pair &P, const double *w, double *out, const int
 }
 
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
-                 cudaStream_t s) {
+                 cudaStream_t s, const double *out_scale) {
   const int nx = C.nx, ny = (C.dim == 2) ? C.ny : 1;
   const int m = nx * ny;
   const int rows = C.n_steps + 1;
   const int64_t N = (int64_t)rows * m;
+  // out_scale (output of the solve for rhs / scale's reciprocal): 2-D FFT path
+  PMK_RETURN_IF(out_scale && !(C.kind == PMK_COARSE_DST && C.fft_x && ny > 1), PMK_ERR_ARG);
   if (C.kind == PMK_COARSE_DST && C.fft_x) {
     // FFT sine transforms (pmk_dst.cu): every pass streams the vector once.
     PMK_RETURN_IF(!C.delta || !C.beta || !C.work0, PMK_ERR_ARG);
@@ -417,7 +422,7 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
         prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
         dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta,
                                                              C.dropped, C.n_steps, m,
-                                                             C.fft_scale, live);
+                                                             C.fft_scale, live, out_scale);
       }
       PMK_LAUNCH_CHECK();
       rc = launch_dst_cols(C.work1, C.work0, nx, ny, rows, C.fft_y, live, s);
@@ -427,7 +432,8 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     }
     {
       prof::Scope cs(prof::kCoarseMisc, 16.0 * m, 0.0, s);
-      copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);  // stepper.py:118
+      copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live,
+                                                      out_scale);  // stepper.py:118
     }
     PMK_LAUNCH_CHECK();
     return 0;

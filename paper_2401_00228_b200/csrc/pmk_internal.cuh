@@ -168,6 +168,13 @@ struct MarchParams {
   double *vh_partials; // optional: per-block partial sums of vh^2 (TMA path only;
                        // launch_march reports 0 partials when it is not produced)
   double *v_norm_out;  // optional: the normalised input v = v_raw / scale
+  // MVR "sub" mode (deferred orthogonalisation, fgmres_fixed): the input is
+  // w - (*v_sub_coef) v_sub, staged together (both level-size); it is stored
+  // into v_norm_out (the next raw basis vector) with per-block partials of
+  // its ||.||^2 in vn_partials; v_scale must be NULL (outputs unscaled).
+  const double *v_sub;
+  const double *v_sub_coef;
+  double *vn_partials;
   // IMV
   const double *vt;
   const int32_t *group_of;
@@ -215,7 +222,7 @@ int mgrit_interpolate(const pmk_pair &P, const double *w, double *out, const int
 int launch_dst_cols(const double *in, double *out, int nx, int ny, int slices,
                     const double *tables, const int *live, cudaStream_t s);
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
-                 cudaStream_t s);
+                 cudaStream_t s, const double *out_scale = nullptr);
 
 // --------------------------------------------------------------- transfer
 int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, const int *live,

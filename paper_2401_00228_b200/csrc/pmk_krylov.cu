@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kRedThreads)
 
 
 // Back substitution (solver.py:442-444).
-__global__ void backsolve_kernel(KState *st, int ld) {
+__global__ void backsolve_kernel(KState *st, int ld, const double *out_scale) {
   if (!st->entered || threadIdx.x != 0) return;
   const int n = st->n_iter;
   const double *h = st->h, *g = st->g;
@@ -587,6 +587,9 @@ __global__ void backsolve_kernel(KState *st, int ld) {
     for (int k = i + 1; k < n; ++k) d = __dadd_rn(d, __dmul_rn(h[i * ld + k], y[k]));
     y[i] = __ddiv_rn(__dsub_rn(g[i], d), h[i * ld + i]);
   }
+  // the caller wants the solution for rhs * out_scale (linear in the rhs)
+  if (out_scale)
+    for (int i = 0; i < n; ++i) y[i] = __dmul_rn(y[i], *out_scale);
 }
 
 // x = sum_i y_i x_i with x_i = v_i - Z vt_i recomputed (solver.py:445-447,
@@ -899,6 +902,15 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
   return 0;
 }
 
+int launch_icwy_solve(KState *st, int ld, int j, const double *c0p, int n_c0,
+                      cudaStream_t s) {
+  PMK_RETURN_IF(j != 0, PMK_ERR_ARG);  // column 0: h_00 = <w, v_0> only
+  prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
+  icwy_solve_kernel<<<1, 1024, sizeof(double), s>>>(st, ld, 0, c0p, n_c0, nullptr, nullptr, 0);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
 int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
                       double tol, cudaStream_t s) {
   prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
@@ -907,9 +919,9 @@ int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_p
   return 0;
 }
 
-int launch_backsolve(KState *st, int ld, cudaStream_t s) {
+int launch_backsolve(KState *st, int ld, cudaStream_t s, const double *out_scale) {
   prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
-  backsolve_kernel<<<1, 32, 0, s>>>(st, ld);
+  backsolve_kernel<<<1, 32, 0, s>>>(st, ld, out_scale);
   PMK_LAUNCH_CHECK();
   return 0;
 }

@@ -60,7 +60,10 @@ int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *v
                     const double *prev, int n_prev, double *partials, cudaStream_t s);
 int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
                       double tol, cudaStream_t s);
-int launch_backsolve(KState *st, int ld, cudaStream_t s);
+int launch_backsolve(KState *st, int ld, cudaStream_t s, const double *out_scale = nullptr);
+// column 0's ICWY solve alone (h_00 = <w, v_0>, hv[0]): the deferred update of
+// fgmres_fixed's fused first step
+int launch_icwy_solve(KState *st, int ld, int j, const double *c0p, int n_c0, cudaStream_t s);
 int launch_assemble(const KState *st, const AssembleArgs &a, double *x, int64_t n, int m, int nu,
                     int m_coarse, const int32_t *group_of, int first, cudaStream_t s);
 

@@ -265,6 +265,7 @@ double march_bytes(int mode, const MarchParams &p, int *cat) {
     *cat = prof::kMVR;
     double b = 8.0 * N + 8.0 * (double)(p.n_steps / p.nu + 1) * p.m;
     if (p.v_norm_out) b += 8.0 * N;
+    if (p.v_sub) b += 8.0 * N;
     return b;
   }
   *cat = prof::kIMV;
@@ -288,6 +289,7 @@ int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials
     const int rc = launch_march_tma(mode, p, s, n_partials, bytes, cat, &handled);
     if (rc || handled) return rc;
   }
+  if (p.v_sub) return PMK_ERR_UNSUPPORTED;  // sub mode: TMA path only
   switch (mode) {
     case kModeMV:
       return dispatch<kModeMV>(p, s, n_partials, bytes, cat);

@@ -112,7 +112,10 @@ template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, b
 __global__ void __launch_bounds__(kTmaThreads)
     march_tma_kernel(const MarchParams p, const __grid_constant__ CUtensorMap tm_v,
                      const __grid_constant__ CUtensorMap tm_vt, const TmaGeom g) {
-  constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
+  // K-MVR "sub" mode (MarchParams::v_sub; GATHER, meaningless for K-MVR,
+  // selects it): the staged input is w - c v_sub, v_sub staged alongside
+  constexpr bool kSub = MODE == kModeMVR && GATHER;
+  constexpr int NB = ((MODE == kModeIMV && !GATHER) || kSub) ? 2 : 1;
   constexpr int ROWS = (DIM == 2) ? R + 2 : 1;
   constexpr int RO = (DIM == 2) ? R : 1;  // output rows per tile
   // TMA tensor destinations must be 128-byte aligned; dynamic shared memory
@@ -162,6 +165,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   // block barrier per slice fewer.
   constexpr bool kLazy = FMA && MODE == kModeMVR && SCALED;
   const double osc = kLazy ? vrcp : 1.0;
+  const double csub = kSub ? *p.v_sub_coef : 0.0;
+  double wsq = 0.0;  // sub mode: ||w - c v_0||^2 of the stored values
   // j = 0 (v is v_0): <w, v_0> takes the staged input itself, no v_0 stream
   const bool v0_self = kPj && p.v0 == p.v;
   // a lazily scaled v_0 (raw rhs, divisor *v0_scale) is scaled at use
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         const int c = (int)((int64_t)k * m + (int64_t)y * nx + boxx);
         tma_row(sv + r * kBox, &tm_v, c & ~1, &bars[stage]);
         if (NB == 2) {
-          const int cv = (int)((int64_t)K * p.m_coarse + (int64_t)y * nx + boxx);
+          const int cv = kSub ? c : (int)((int64_t)K * p.m_coarse + (int64_t)y * nx + boxx);
           tma_row(sv + (ROWS + r) * kBox, &tm_vt, cv & ~1, &bars[stage]);
         }
       }
@@ -303,8 +308,8 @@ __global__ void __launch_bounds__(kTmaThreads)
       }
       mbar_wait(&bars[stage], (it / S) & 1);
       // ---- pre-pass: u = v / scale  or  u = v - Z vt, once per element
-      if (((SCALED && !kLazy) || MODE == kModeIMV) && pin) {
-        const double *vtk = GATHER ? p.vt + (int64_t)K * p.m_coarse : nullptr;
+      if (((SCALED && !kLazy) || MODE == kModeIMV || kSub) && pin) {
+        const double *vtk = (GATHER && !kSub) ? p.vt + (int64_t)K * p.m_coarse : nullptr;
 #pragma unroll
         for (int r = 0; r < ROWS; ++r) {
           if (r < rlo || r > rhi) continue;
@@ -318,10 +323,12 @@ __global__ void __launch_bounds__(kTmaThreads)
                                     : sv[(ROWS + r) * kBox + pe + ((pK + (y & nx)) & 1)];
             u = __dsub_rn(u, z);
           }
+          if (kSub)  // w - c v_0, the update pass's per-element rounding
+            u = __dsub_rn(u, __dmul_rn(csub, sv[(ROWS + r) * kBox + pe + ((pk + (y & nx)) & 1)]));
           *cell = u;
         }
       }
-      if ((SCALED && !kLazy) || MODE == kModeIMV) __syncthreads();
+      if ((SCALED && !kLazy) || MODE == kModeIMV || kSub) __syncthreads();
       // ---- stencil pass, mask-free variant: every neighbour exists, k >= 1,
       // no dropped coupling.  Tile rows start at even y0 (R even) and box row
       // r holds grid row y0 - 1 + r, odd for even r: its parity shift
@@ -372,6 +379,7 @@ __global__ void __launch_bounds__(kTmaThreads)
               p.out[gi] = o;
             } else if (MODE == kModeMVR) {
               if (wn) ob[r * nx] = kLazy ? __dmul_rn(cur, osc) : cur;
+              if (kSub) wsq = fma(cur, cur, wsq);
               const double sval = FMA ? fma(-p.mu, cur, o) : __dsub_rn(o, __dmul_rn(p.mu, cur));
               if (inj) {
                 if (k % nu == 0) {
@@ -451,6 +459,7 @@ __global__ void __launch_bounds__(kTmaThreads)
               p.out[kofs + gi] = o;
             } else if (MODE == kModeMVR) {
               if (has_vn) p.v_norm_out[kofs + gi] = kLazy ? __dmul_rn(cur, osc) : cur;
+              if (kSub) wsq = fma(cur, cur, wsq);
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
               if (p.inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
                 if (k % nu == 0) {
@@ -511,6 +520,10 @@ __global__ void __launch_bounds__(kTmaThreads)
   if (MODE == kModeMVR && p.vh_partials) {
     const double s = block_sum(vsq);
     if (threadIdx.x == 0) p.vh_partials[blockIdx.x] = s;
+  }
+  if (kSub) {
+    const double s = block_sum(wsq);
+    if (threadIdx.x == 0) p.vn_partials[blockIdx.x] = s;
   }
 }
 
@@ -776,7 +789,7 @@ bool encode_1d(CUtensorMap *map, const double *base, int64_t n) {
 template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA = false>
 int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
             int *n_partials, double bytes, int cat) {
-  constexpr int NB = (MODE == kModeIMV && !GATHER) ? 2 : 1;
+  constexpr int NB = ((MODE == kModeIMV && !GATHER) || (MODE == kModeMVR && GATHER)) ? 2 : 1;
   constexpr int ROWS = (DIM == 2) ? R + 2 : R;
   const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
   auto kern = (DIM == 2) ? march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED, FMA>
@@ -848,6 +861,8 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
   if (mode == kModeIMV && !gather) {
     const int64_t Nc = (int64_t)(p.n_steps / p.nu + 1) * p.m_coarse;
     if (!encode_1d(&mvt, p.vt, Nc)) return 0;
+  } else if (mode == kModeMVR && p.v_sub) {
+    if (!encode_1d(&mvt, p.v_sub, N)) return 0;
   } else {
     mvt = mv;
   }
@@ -889,6 +904,14 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
       else PMK_RUN(kModeMV, 1, 1, 8, false);
       break;
     case kModeMVR:
+      if (p.v_sub) {  // sub mode: 2-D, constant stencils, in-solver, unscaled only
+        if (!(d2 && p.fma && !var && !scaled && !p.dropped && p.v_norm_out && p.vn_partials &&
+              p.v_sub_coef))
+          return PMK_ERR_ARG;
+        rc = run_tma<kModeMVR, 2, 4, 2, false, true, false, true>(p, mv, mvt, s, n_partials, bytes,
+                                                                   cat);
+        break;
+      }
       if (d2) {
         if (p.fma && !var && scaled && !p.dropped && (cfg_mvr == 0 || cfg_mvr >= 4)) {
           // in-solver K-MVR: 8-row tiles x 3 stages (no pre-pass since the lazy
