@@ -908,8 +908,16 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
         if (!(d2 && p.fma && !var && !scaled && !p.dropped && p.v_norm_out && p.vn_partials &&
               p.v_sub_coef))
           return PMK_ERR_ARG;
-        rc = run_tma<kModeMVR, 2, 4, 2, false, true, false, true>(p, mv, mvt, s, n_partials, bytes,
-                                                                   cat);
+        static const bool tall = [] {  // PMK_SUB_TALL=1: 8-row tiles (2 CTAs/SM)
+          const char *e = getenv("PMK_SUB_TALL");
+          return e && e[0] == '1';
+        }();
+        if (tall)
+          rc = run_tma<kModeMVR, 2, 8, 2, false, true, false, true>(p, mv, mvt, s, n_partials,
+                                                                     bytes, cat);
+        else
+          rc = run_tma<kModeMVR, 2, 4, 2, false, true, false, true>(p, mv, mvt, s, n_partials,
+                                                                     bytes, cat);
         break;
       }
       if (d2) {
