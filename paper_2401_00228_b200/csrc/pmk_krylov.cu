@@ -854,7 +854,11 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
   case C:                                       \
     dots_vec<C>(st, w, v[j], V, n, part, s);    \
     break;
+#if PMK_DOT_GROUP > 8
+        PMK_CASES16(PMK_DOTS_CASE)
+#else
         PMK_CASES8(PMK_DOTS_CASE)
+#endif
 #undef PMK_DOTS_CASE
         default:
           return PMK_ERR_ARG;

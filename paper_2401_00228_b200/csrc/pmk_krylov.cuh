@@ -39,7 +39,10 @@ struct AssembleArgs {
 };
 
 constexpr int kGroup = 16;     // basis vectors per ICWY update pass
-constexpr int kDotGroup = 8;   // basis vectors per ICWY dot pass (ptxas serialises
+#ifndef PMK_DOT_GROUP
+#define PMK_DOT_GROUP 8
+#endif
+constexpr int kDotGroup = PMK_DOT_GROUP;  // basis vectors per ICWY dot pass (ptxas serialises
                                // the loads of larger groups: ~3 TB/s at 12)
 struct MultiVec {
   const double *v[kGroup];
