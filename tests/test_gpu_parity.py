@@ -241,6 +241,22 @@ def test_host_output_slabs_bitwise(name):
         assert ro.outer_iterations == rd.outer_iterations
 
 
+@pytest.mark.parametrize("budgets", [(3, 2, 1), (2, 3, 2), (4, 1, 2)])
+def test_inner_budgets_vs_oracle(budgets):
+    """Fixed inner budgets other than the default [2, 2, 1] (SolverConfig
+    inner_iters, solver.py:219-235) against the CPU oracle: exercises the
+    deferred first orthogonalisation of fgmres_fixed with budgets > 2 (step 1
+    writing into slot 2) and a budget-1 level between fused ones."""
+    from oracle import pintmk_oracle as O
+    from paper_2401_00228_b200 import multilevel_solve
+
+    case = SMALL["c5_small"].scaled(inner_iters=budgets)
+    x, rep = multilevel_solve(gpu_hierarchy(case))
+    xo, info = O.solve(oracle_hierarchy(case))
+    assert abs(rep.outer_iterations - info["iterations"]) <= 1
+    assert rel(x, xo) <= 1e-10, rel(x, xo)
+
+
 @pytest.mark.parametrize("name", ["c5_small", "c4_small", "mgrit2_small", "c2_small"])
 def test_lazy_basis_matches_normalised_basis(name):
     """The lazy Krylov basis (default) against the explicitly normalised one
