@@ -130,6 +130,7 @@ struct LevelRT {
   const int *parent_live = nullptr;
   // pinned ring of KState snapshots (pmk_fgmres_snapshot / _read)
   KState *snap = nullptr;
+  int ugram_col = -1;  // column whose Gram row the last update pass produced
 };
 
 }  // namespace
@@ -298,7 +299,8 @@ int alloc_state(LevelRT &R, int cap) {
   const size_t n_groups = (size_t)(cap + kDotGroup - 1) / kDotGroup;
   const size_t n_dotp = n_groups * (2 * kDotGroup + 1) * kMaxPartials;
   const size_t n_doubles =
-      2 * nh + (size_t)cap * cap + 8 * (size_t)(cap + 1) + 4 * kMaxPartials + n_dotp;
+      2 * nh + (size_t)cap * cap + 8 * (size_t)(cap + 1) + 4 * kMaxPartials + n_dotp +
+      (size_t)(cap + 1) * kMaxPartials;
   const size_t bytes = sizeof(KState) + 64 + n_doubles * sizeof(double);
   PMK_CUDA_TRY(cudaMalloc(&R.d_block, bytes));
   PMK_CUDA_TRY(cudaMemset(R.d_block, 0, bytes));
@@ -326,6 +328,8 @@ int alloc_state(LevelRT &R, int cap) {
   d += cap + 1;
   h.hv = d;
   d += cap + 1;
+  h.ugp = d;
+  d += (size_t)(cap + 1) * kMaxPartials;
   h.lazy = lazy_basis() ? 1 : 0;
   R.partA = d;  // K-IMV <w, v_0>, then the pj block (<w, v_j>, <v_j, v_0>)
   d += 3 * kMaxPartials;
@@ -367,6 +371,7 @@ int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double t
   R.rhs_cur = rhs;
   R.pending = rhs;
   R.v.clear();
+  R.ugram_col = -1;
   R.vt.clear();
   return 0;
 }
@@ -562,9 +567,19 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     // the last step of a fixed-budget inner solve needs only ||w||, not w
     int n_norm = 0;
     bool finished = false;  // (finish_col fused into the last update pass)
+    // Gram row of v_{j+1} out of this column's update pass (lazy basis: raw
+    // products, scaled in the next ICWY solve), used by the next column
+    static const bool ugram_on = [] {
+      const char *e = getenv("PMK_UGRAM");
+      return !(e && e[0] == '0');
+    }();
+    const bool ug_in = ugram_on && lazy && R.ugram_col == j;
+    const bool ug_out = ugram_on && lazy && keep_w && j + 1 < R.cap;
+    bool ug_done = false;
     rc = launch_icwy_mgs(R.d_state, R.cap, j, w_next, R.v.data(), R.N, R.partA, np,
                          pj_done ? pj : nullptr, R.partM, R.partB, &n_norm, keep_w, s, R.tol,
-                         true, &finished);
+                         true, &finished, ug_in, ug_out, &ug_done);
+    R.ugram_col = ug_done ? j + 1 : -1;
     if (rc) return rc;
     if (!finished) rc = launch_finish_col(R.d_state, R.cap, j, R.partB, n_norm, R.tol, s);
     if (rc) return rc;

@@ -321,6 +321,52 @@ __global__ void __launch_bounds__(kRedThreads)
   block_sum_multi<1>(awj, out + (int64_t)2 * kDotGroup * gridDim.x, gridDim.x);
 }
 
+// <w, v_q> only (slot q at partials[q * gridDim.x]), up to kGroup vectors:
+// the Gram row of v_j came from the update pass that produced v_j.
+template <int CNT>
+__global__ void __launch_bounds__(kRedThreads)
+    icwy_dotsw_vec_kernel(const KState *st, const double *__restrict__ w, MultiVec V, int64_t n,
+                          double *partials) {
+  if (!st->live) return;
+  constexpr int U = (12 / (CNT + 1)) > 1 ? 12 / (CNT + 1) : 1;
+  double aw[CNT];
+#pragma unroll
+  for (int q = 0; q < CNT; ++q) aw[q] = 0.0;
+  const double2 *w2 = reinterpret_cast<const double2 *>(w);
+  const double2 *c2[CNT];
+#pragma unroll
+  for (int q = 0; q < CNT; ++q) c2[q] = reinterpret_cast<const double2 *>(V.v[q]);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n2 = n >> 1;
+  int64_t i = t0;
+  for (; i + (U - 1) * stride < n2; i += U * stride) {
+    double2 a[U], c[U][CNT];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      a[u] = __ldg(w2 + i + u * stride);
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) c[u][q] = __ldg(c2[q] + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) aw[q] = dot2(aw[q], a[u], c[u][q]);
+    }
+  }
+  for (; i < n2; i += stride) {
+    const double2 a = __ldg(w2 + i);
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) aw[q] = dot2(aw[q], a, __ldg(c2[q] + i));
+  }
+  if ((n & 1) && t0 == stride - 1) {
+    const double a = w[n - 1];
+#pragma unroll
+    for (int q = 0; q < CNT; ++q) aw[q] = __dadd_rn(aw[q], __dmul_rn(a, V.v[q][n - 1]));
+  }
+  block_sum_multi<CNT>(aw, partials + blockIdx.x, gridDim.x);
+}
+
 // Any alignment, runtime group size.
 __global__ void __launch_bounds__(kRedThreads)
     icwy_dots_kernel(const KState *st, const double *__restrict__ w,
@@ -369,7 +415,7 @@ __device__ __forceinline__ double warp_reduce_partials(const double *p, int n) {
 //   (pj + kMaxPartials) and the group passes start at v_1.
 __global__ void __launch_bounds__(1024)
     icwy_solve_kernel(KState *st, int ld, int j, const double *c0p, int n_c0,
-                      const double *pj, const double *gp, int n_gp) {
+                      const double *pj, const double *gp, int n_gp, int ugram = 0) {
   if (!st->live) return;
   extern __shared__ double sh[];  // c[0..j], g[0..j-1]
   double *c = sh, *g = sh + (j + 1);
@@ -380,6 +426,11 @@ __global__ void __launch_bounds__(1024)
     double x;
     if (d == 0) {
       x = warp_reduce_partials(c0p, n_c0);
+    } else if (d < j && ugram) {  // w-only dot passes, kGroup slots per pass
+      const int e = d - 1;
+      x = warp_reduce_partials(gp + (int64_t)(e / kGroup) * kGroup * n_gp + (e % kGroup) * n_gp,
+                               n_gp);
+      x = __dmul_rn(x, st->vrcp[d]);
     } else if (d < j) {  // <w, v_d>, 1 <= d < j (dot pass: raw v_d)
       const int e = d - o;
       x = warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride + (e % kDotGroup) * n_gp, n_gp);
@@ -391,6 +442,10 @@ __global__ void __launch_bounds__(1024)
     } else {  // <v_j, v_i>, i = d - j - 1
       const int i = d - j - 1;
       const int e = i - o;
+      if (ugram && i >= 1) {  // from the update pass that produced v_j (raw x raw)
+        x = __dmul_rn(warp_reduce_partials(st->ugp + (int64_t)i * kMaxPartials, kRedBlocks),
+                      __dmul_rn(st->vrcp[j], st->vrcp[i]));
+      } else
       x = (pj && i == 0)
               ? warp_reduce_partials(pj + kMaxPartials, n_c0)
               : __dmul_rn(warp_reduce_partials(gp + (int64_t)(e / kDotGroup) * gstride +
@@ -482,7 +537,7 @@ __global__ void finish_col_kernel(KState *st, int ld, int j, const double *parti
 
 // w -= sum_q h[i0+q][j] v_q (ascending q, the reference's per-element
 // rounding); with `partials`, the partial sums of ||w||^2 of the result.
-template <int CNT>
+template <int CNT, bool GRAM = false>
 __global__ void __launch_bounds__(kRedThreads)
     icwy_update_vec_kernel(KState *st, int ld, int j, int i0, MultiVec V,
                            double *__restrict__ w, int64_t n, double *partials, bool store,
@@ -497,6 +552,9 @@ __global__ void __launch_bounds__(kRedThreads)
     c2[q] = reinterpret_cast<const double2 *>(V.v[q]);
   }
   double acc[1] = {0.0};
+  double ag[GRAM ? CNT : 1];  // GRAM: <w', raw_q>, the next basis vector's Gram row
+#pragma unroll
+  for (int q = 0; q < (GRAM ? CNT : 1); ++q) ag[q] = 0.0;
   double2 *w2 = reinterpret_cast<double2 *>(w);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -519,6 +577,10 @@ __global__ void __launch_bounds__(kRedThreads)
       }
       if (store) w2[i + u * stride] = a[u];
       if (partials) acc[0] = dot2(acc[0], a[u], a[u]);
+      if constexpr (GRAM) {
+#pragma unroll
+        for (int q = 0; q < CNT; ++q) ag[q] = dot2(ag[q], a[u], c[u][q]);
+      }
     }
   }
   for (; i < n2; i += stride) {
@@ -531,6 +593,10 @@ __global__ void __launch_bounds__(kRedThreads)
     }
     if (store) w2[i] = a;
     if (partials) acc[0] = dot2(acc[0], a, a);
+    if constexpr (GRAM) {
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) ag[q] = dot2(ag[q], a, __ldg(c2[q] + i));
+    }
   }
   if ((n & 1) && t0 == stride - 1) {
     double a = w[n - 1];
@@ -538,6 +604,14 @@ __global__ void __launch_bounds__(kRedThreads)
     for (int q = 0; q < CNT; ++q) a = __dsub_rn(a, __dmul_rn(hq[q], V.v[q][n - 1]));
     if (store) w[n - 1] = a;
     if (partials) acc[0] = __dadd_rn(acc[0], __dmul_rn(a, a));
+    if constexpr (GRAM) {
+#pragma unroll
+      for (int q = 0; q < CNT; ++q) ag[q] = __dadd_rn(ag[q], __dmul_rn(a, V.v[q][n - 1]));
+    }
+  }
+  if constexpr (GRAM) {
+    block_sum_multi<CNT>(ag, st->ugp + (int64_t)i0 * kMaxPartials + blockIdx.x, kMaxPartials);
+    __syncthreads();
   }
   if (partials) block_sum_multi<1>(acc, partials + blockIdx.x, gridDim.x);
   if (finish) {  // last block to finish runs finish_col (fixed-order reduction)
@@ -818,9 +892,19 @@ void dots_vec(const KState *st, const double *w, const double *vj, const MultiVe
 }
 template <int CNT>
 void update_vec(KState *st, int ld, int j, int i0, const MultiVec &V, double *w, int64_t n,
-                double *partials, bool store, bool finish, double tol, cudaStream_t s) {
-  icwy_update_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, ld, j, i0, V, w, n,
-                                                                 partials, store, finish, tol);
+                double *partials, bool store, bool finish, double tol, cudaStream_t s,
+                bool gram = false) {
+  if (gram)
+    icwy_update_vec_kernel<CNT, true><<<kRedBlocks, kRedThreads, 0, s>>>(
+        st, ld, j, i0, V, w, n, partials, store, finish, tol);
+  else
+    icwy_update_vec_kernel<CNT, false><<<kRedBlocks, kRedThreads, 0, s>>>(
+        st, ld, j, i0, V, w, n, partials, store, finish, tol);
+}
+template <int CNT>
+void dotsw_vec(const KState *st, const double *w, const MultiVec &V, int64_t n,
+               double *partials, cudaStream_t s) {
+  icwy_dotsw_vec_kernel<CNT><<<kRedBlocks, kRedThreads, 0, s>>>(st, w, V, n, partials);
 }
 
 #define PMK_CASES8(F) F(1) F(2) F(3) F(4) F(5) F(6) F(7) F(8)
@@ -832,16 +916,39 @@ void update_vec(KState *st, int ld, int j, int i0, const MultiVec &V, double *w,
 int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
                     const double *c0p, int n_c0, const double *pj, double *dot_partials,
                     double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s, double tol,
-                    bool fuse_finish, bool *finished) {
+                    bool fuse_finish, bool *finished, bool ugram_in, bool ugram_out,
+                    bool *ugram_done) {
   if (finished) *finished = false;
+  if (ugram_done) *ugram_done = false;
   auto al = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   bool vec = al(w);
   for (int i = 0; i <= j; ++i) vec = vec && al(v[i]);
   const int64_t gstride = (int64_t)(2 * kDotGroup + 1) * kRedBlocks;
   if (j < 1) pj = nullptr;
+  const bool ug = ugram_in && vec && pj && j >= 2;
+  // ug: the Gram row of v_j is already in st->ugp; the dot passes need
+  // <w, v_i>, 0 < i < j, only (w and up to kGroup basis vectors per pass)
+  for (int i0 = 1, gi = 0; ug && i0 < j; i0 += kGroup, ++gi) {
+    const int cnt = (j - i0 < kGroup) ? j - i0 : kGroup;
+    MultiVec V{};
+    for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
+    prof::Scope scope(prof::kMGS, 8.0 * (cnt + 1) * (double)n, 4.0 * cnt * (double)n, s);
+    double *part = dot_partials + (int64_t)gi * kGroup * kRedBlocks;
+    switch (cnt) {
+#define PMK_DOTSW_CASE(C)                   \
+  case C:                                   \
+    dotsw_vec<C>(st, w, V, n, part, s);     \
+    break;
+      PMK_CASES16(PMK_DOTSW_CASE)
+#undef PMK_DOTSW_CASE
+      default:
+        return PMK_ERR_ARG;
+    }
+    PMK_LAUNCH_CHECK();
+  }
   // with pj the K-IMV pass already produced every dot involving v_0 or v_j
   // except the Gram entries <v_j, v_i>, 0 < i < j
-  for (int i0 = pj ? 1 : 0, gi = 0; i0 < j; i0 += kDotGroup, ++gi) {
+  for (int i0 = pj ? 1 : 0, gi = 0; !ug && i0 < j; i0 += kDotGroup, ++gi) {
     const int cnt = (j - i0 < kDotGroup) ? j - i0 : kDotGroup;
     MultiVec V{};
     for (int q = 0; q < cnt; ++q) V.v[q] = v[i0 + q];
@@ -870,8 +977,8 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
   }
   {
     prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
-    icwy_solve_kernel<<<1, 1024, (2 * j + 1) * sizeof(double), s>>>(st, ld, j, c0p, n_c0, pj,
-                                                                   dot_partials, kRedBlocks);
+    icwy_solve_kernel<<<1, 1024, (2 * j + 1) * sizeof(double), s>>>(
+        st, ld, j, c0p, n_c0, pj, dot_partials, kRedBlocks, ug ? 1 : 0);
     PMK_LAUNCH_CHECK();
   }
   for (int i0 = 0; i0 <= j; i0 += kGroup) {
@@ -882,6 +989,9 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
     const bool store = keep_w || !last;
     const bool fin = last && fuse_finish && vec;
     if (fin && finished) *finished = true;
+    // one pass over all of v_0..v_j: it can leave the next vector's Gram row
+    const bool gram = ugram_out && vec && store && i0 == 0 && last;
+    if (gram && ugram_done) *ugram_done = true;
     prof::Scope scope(prof::kMGS, 8.0 * (cnt + (store ? 2 : 1)) * (double)n,
                       2.0 * (cnt + (last ? 1 : 0)) * (double)n, s);
     double *part = last ? norm_partials : nullptr;
@@ -889,7 +999,7 @@ int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v
       switch (cnt) {
 #define PMK_UPD_CASE(C)                                \
   case C:                                              \
-    update_vec<C>(st, ld, j, i0, V, w, n, part, store, fin, tol, s); \
+    update_vec<C>(st, ld, j, i0, V, w, n, part, store, fin, tol, s, gram); \
     break;
         PMK_CASES16(PMK_UPD_CASE)
 #undef PMK_UPD_CASE

@@ -22,6 +22,9 @@ struct KState {
   double *hv;  // current column's update coefficients h_i * vrcp_i (ICWY)
   int lazy;
   unsigned int ticket;  // blocks done in a pass that ends with a fused finish
+  // Gram row of the next basis vector, accumulated by the update pass that
+  // produces it: partials of <w', raw_i> at ugp[i * kMaxPartials + block]
+  double *ugp;
   double *hist;    // residual history rel_j
   double *gram;    // cap x cap, row i = <v_i, v_l>, l < i (ICWY MGS)
   double beta, rel;
@@ -51,10 +54,15 @@ struct MultiVec {
 // With fuse_finish (and aligned operands) the last block of the last update
 // pass also runs finish_col (h[j+1][j], Givens, stop test); *finished tells
 // the caller whether it still has to launch it.
+// ugram_in: the Gram row of v_j was produced by the previous update pass
+// (the dot passes then read w and v_1..v_{j-1} only, 16 vectors per pass);
+// ugram_out: this column's single update pass produces the Gram row of the
+// next basis vector.  *ugram_done reports whether it did.
 int launch_icwy_mgs(KState *st, int ld, int j, double *w, const double *const *v, int64_t n,
                     const double *c0p, int n_c0, const double *pj, double *dot_partials,
                     double *norm_partials, int *n_norm, bool keep_w, cudaStream_t s,
-                    double tol = 0.0, bool fuse_finish = false, bool *finished = nullptr);
+                    double tol = 0.0, bool fuse_finish = false, bool *finished = nullptr,
+                    bool ugram_in = false, bool ugram_out = false, bool *ugram_done = nullptr);
 
 int launch_begin(KState *st, const double *partials, int n_partials, const int *parent_live,
                  cudaStream_t s);
