@@ -269,7 +269,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
 int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double *v_scale,
            const double *vt, double *x, double *w, const double *v0, const double *v0_scale,
            double *partials, int *n_partials, const int *live, cudaStream_t s,
-           bool fused = false, double *pj = nullptr, int *pj_done = nullptr) {
+           bool fused = false, double *pj = nullptr, int *pj_done = nullptr, int pj_wsq = 0) {
   MarchParams p = base_params(L);
   p.fma = fused ? 1 : 0;
   p.v = v;
@@ -285,6 +285,7 @@ int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double 
   p.partials = partials;
   p.pj = pj;
   p.pj_done = pj_done;
+  p.pj_wsq = pj_wsq;
   p.live = live;
   return launch_march(kModeIMV, p, s, n_partials);
 }
@@ -484,7 +485,7 @@ int mvr_into_child(pmk_hier *H, int idx, const double *v, const double *v_scale,
 // fuse (fgmres_fixed only): kStepDefer = step 0 stops after h_00 (its w stays
 // unorthogonalised in w_next); kStepSub = step 1 starts with the deferred
 // update, fused into its K-MVR, which stores v_1 raw into sub_store.
-constexpr int kStepPlain = 0, kStepDefer = 1, kStepSub = 2;
+constexpr int kStepPlain = 0, kStepDefer = 1, kStepSub = 2, kStepPyth = 3;
 
 int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, double *child_out,
                 cudaStream_t s, bool keep_w = true, int fuse = kStepPlain,
@@ -550,11 +551,21 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     const char *e = getenv("PMK_PJ");
     return !(e && e[0] == '0');
   }();
-  double *pj = (j >= 1 && !classic_mgs() && pj_on) ? R.partA + kMaxPartials : nullptr;
+  const bool pyth = fuse == kStepPyth && j == 0;  // (budget 1: ||w||^2 instead)
+  double *pj = ((j >= 1 || pyth) && !classic_mgs() && pj_on) ? R.partA + kMaxPartials : nullptr;
   rc = do_imv(R.L, R.P, R.v[j], lazy ? K.vscale + j : nullptr, child_out, nullptr, w_next,
               R.v[0], lazy ? K.vscale : nullptr, R.partA, &np, live, s, !classic_mgs(), pj,
-              &pj_done);
+              &pj_done, pyth ? 1 : 0);
   if (rc) return rc;
+  if (pyth && pj_done) {  // one-column solve: h_00, then h_10 from ||w||^2
+    rc = launch_icwy_solve(R.d_state, R.cap, 0, R.partA, np, s);
+    if (rc) return rc;
+    rc = launch_finish_col(R.d_state, R.cap, 0, pj, np, R.tol, s, true);
+    if (rc) return rc;
+    R.pending = w_next;
+    R.vt.push_back(child_out);
+    return 0;
+  }
   if (fuse == kStepDefer) {  // h_00 only; update + finish_col(0) follow in step 1
     rc = launch_icwy_solve(R.d_state, R.cap, 0, R.partA, np, s);
     if (rc) return rc;
@@ -681,13 +692,18 @@ int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaSt
   const bool fuse = fuse01() && lazy && R.budget >= 2 && !R.P.mgrit && !R.P.group_of &&
                     R.L.dim == 2 && !R.L.diag_t.var && !R.L.sub_t.var && !R.L.dropped &&
                     child_scalable(H, idx);
+  // budget 1: no update pass at all (h_10 from ||w||^2, see finish_col_block)
+  const bool pyth1 = fuse01() && lazy && R.budget == 1 && !R.P.mgrit && !R.P.group_of &&
+                     R.L.dim == 2 && !R.L.diag_t.var && !R.L.sub_t.var && !R.L.dropped;
   for (int j = 0; j < R.budget; ++j) {
     // lazy basis: v_0 is the rhs, step j's w goes to slot j+1 (it is basis
     // vector j+1), the last step's w only feeds ||w|| (w_buf)
     double *w_next = (lazy && j + 1 < R.budget) ? R.v_slots[j + 1] : R.w_buf;
     int mode = kStepPlain;
     double *store = nullptr;
-    if (fuse && j == 0) {
+    if (pyth1) {
+      mode = kStepPyth;
+    } else if (fuse && j == 0) {
       mode = kStepDefer;
       w_next = R.w_buf;  // w_0 raw, consumed by step 1's K-MVR
     } else if (fuse && j == 1) {

@@ -189,6 +189,9 @@ struct MarchParams {
   // only; the launcher reports whether it did in *pj_done (host pointer).
   double *pj;
   int *pj_done;
+  // with pj and v == v0 (j = 0): slot 0 receives ||w||^2 partials instead
+  // (budget-1 inner levels: h_10^2 = ||w||^2 - h_00^2, no update pass)
+  int pj_wsq;
   const int *live;
 };
 

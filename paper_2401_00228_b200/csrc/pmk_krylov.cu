@@ -487,9 +487,14 @@ __global__ void __launch_bounds__(1024)
 // one block (all its threads take part in the reduction).
 __device__ __forceinline__ void finish_col_block(KState *st, int ld, int j,
                                                  const double *partials, int n_partials,
-                                                 double tol) {
-  const double ss = reduce_partials(partials, n_partials);
+                                                 double tol, bool pyth = false) {
+  double ss = reduce_partials(partials, n_partials);
   if (threadIdx.x != 0) return;
+  // pyth (column 0 of a budget-1 solve): the partials are ||w||^2 of the
+  // unorthogonalised w; ||w - h_00 v_0||^2 = ||w||^2 - h_00^2.  Only
+  // h_00^2 + h_10^2 = ||w||^2 enters the one-column least squares (y_0 =
+  // beta h_00 / ||w||^2), so the cancellation for h_10 << ||w|| does not.
+  if (pyth) ss = fmax(__dsub_rn(ss, __dmul_rn(st->h[0], st->h[0])), 0.0);
   double *h = st->h;
   const double hn = sqrt(ss);
   h[(j + 1) * ld + j] = hn;
@@ -530,9 +535,9 @@ __device__ __forceinline__ void finish_col_block(KState *st, int ld, int j,
 }
 
 __global__ void finish_col_kernel(KState *st, int ld, int j, const double *partials,
-                                  int n_partials, double tol) {
+                                  int n_partials, double tol, bool pyth = false) {
   if (!st->live) return;
-  finish_col_block(st, ld, j, partials, n_partials, tol);
+  finish_col_block(st, ld, j, partials, n_partials, tol, pyth);
 }
 
 // w -= sum_q h[i0+q][j] v_q (ascending q, the reference's per-element
@@ -1026,9 +1031,10 @@ int launch_icwy_solve(KState *st, int ld, int j, const double *c0p, int n_c0,
 }
 
 int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
-                      double tol, cudaStream_t s) {
+                      double tol, cudaStream_t s, bool pyth) {
+  PMK_RETURN_IF(pyth && j != 0, PMK_ERR_ARG);
   prof::Scope scope(prof::kSmall, 0.0, 0.0, s);
-  finish_col_kernel<<<1, kRedThreads, 0, s>>>(st, ld, j, partials, n_partials, tol);
+  finish_col_kernel<<<1, kRedThreads, 0, s>>>(st, ld, j, partials, n_partials, tol, pyth);
   PMK_LAUNCH_CHECK();
   return 0;
 }

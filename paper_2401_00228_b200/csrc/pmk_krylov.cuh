@@ -69,8 +69,9 @@ int launch_begin(KState *st, const double *partials, int n_partials, const int *
 int launch_mgs_pass(KState *st, int ld, int l, int j, double *w, const double *vl,
                     const double *vl_scale, const double *vn, const double *vn_scale, int64_t n,
                     const double *prev, int n_prev, double *partials, cudaStream_t s);
+// pyth: column 0 from ||w||^2 partials (see finish_col_block)
 int launch_finish_col(KState *st, int ld, int j, const double *partials, int n_partials,
-                      double tol, cudaStream_t s);
+                      double tol, cudaStream_t s, bool pyth = false);
 int launch_backsolve(KState *st, int ld, cudaStream_t s, const double *out_scale = nullptr);
 // column 0's ICWY solve alone (h_00 = <w, v_0>, hv[0]): the deferred update of
 // fgmres_fixed's fused first step

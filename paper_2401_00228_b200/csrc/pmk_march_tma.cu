@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   double dwj = 0.0, dgj = 0.0;  // K-IMV with pj: <w, v>, <v, v0>
   // (in-solver variant only; run_tma reports it through p.pj_done)
   constexpr bool kPj = MODE == kModeIMV && DIM == 2 && FMA && !VAR && !GATHER;
-  const bool wantj = kPj && p.pj != nullptr;
+  const bool wantj = kPj && p.pj != nullptr && !p.pj_wsq;
+  const bool wantw = kPj && p.pj != nullptr && p.pj_wsq;  // ||w||^2 into slot 0
   // In-solver (FMA) launches honour a fixed contract, checked by the
   // launcher: K-IMV writes w (p.out) and the <w, v_0> partials and no x;
   // K-MVR writes the normalised v (p.v_norm_out).  Compile-time flags keep
@@ -403,6 +404,8 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
                 dgj = fma(vj[r], v0r, dgj);
+              } else if (wantw) {
+                dwj = fma(o, o, dwj);
               }
             }
           }
@@ -485,6 +488,8 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (wantj) {
                 dwj = fma(o, vj[r], dwj);
                 dgj = fma(vj[r], v0r, dgj);
+              } else if (wantw) {
+                dwj = fma(o, o, dwj);
               }
             }
           }
@@ -509,7 +514,7 @@ __global__ void __launch_bounds__(kTmaThreads)
     const double s = block_sum(dot);
     if (threadIdx.x == 0) p.partials[blockIdx.x] = s;
   }
-  if (wantj) {
+  if (wantj || wantw) {
     const double a = block_sum(dwj);
     const double b = block_sum(dgj);
     if (threadIdx.x == 0) {
