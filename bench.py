@@ -283,6 +283,13 @@ def run_ours(args):
                 "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                 "traffic": traffic, "bytes_per_launch": k["bytes"] / k["launches"],
                 "peak_source": peak_kind,
+                # DRAM rate implied by the ncu per-launch traffic and this run's mean
+                # launch time; frac can exceed 1 because the peak is a copy (50/50
+                # read/write) figure while the Gram/dot passes are read-dominated
+                # (read-only streams sustain ~7.0 TB/s), and inner-level vectors
+                # (<= 266 MB) are partly served from the 126 MB L2 (traffic < alg. bytes)
+                "dram_achieved": (round(traffic / (k["ms"] / k["launches"] / 1000.0) / 1e9, 1)
+                                  if traffic else None),
                 "timing": "CUDA events around every launch on its stream, over a second "
                           "pass of the same K steps right after the timed region"}
 
