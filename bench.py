@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the extra workload lines (other BASELINE shapes)")
+    ap.add_argument("--no-full-shape-cpu", action="store_true",
+                    help="reference arm: skip the one-iteration CPU run on the full shape")
     return ap.parse_args()
 
 
@@ -140,12 +144,30 @@ def cpu_desc(case, info):
             f"OpenBLAS default threads")
 
 
+def cpu_full_shape_iteration(name: str):
+    """One outer FGMRES iteration of the CPU oracle on the workload's own
+    inputs (full shape; the reference's wall_time, solver.py:463-467, for one
+    iteration).  Returns (seconds for the iteration, setup seconds)."""
+    from oracle import pintmk_oracle as O
+    from tests.cases import BASELINE, oracle_hierarchy
+
+    case = BASELINE[name].scaled(max_outer=1, restart=None)
+    t0 = time.perf_counter()
+    h = oracle_hierarchy(case)
+    t1 = time.perf_counter()
+    O.fgmres(h, 0, h.rhs.ravel(), None, 1)
+    t2 = time.perf_counter()
+    del h
+    gc.collect()
+    return t2 - t1, t1 - t0
+
+
 def run_reference(args):
     rank, world, _ = dist_info()
     if rank != 0:
         return
     vals = []
-    for _ in range(min(args.warmup, 1)):
+    for _ in range(max(args.warmup, 0)):
         cpu_sample_solve()
     for _ in range(args.steps):
         v, dt, info, case = cpu_sample_solve()
@@ -154,7 +176,7 @@ def run_reference(args):
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1),
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": max(args.warmup, 0),
         "ms_per_step": 1000.0 * case.N / value, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.case, "sample": CPU_SAMPLE},
@@ -162,7 +184,31 @@ def run_reference(args):
                          "sample": cpu_desc(case, info)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_full_shape_cpu:
+        from tests.cases import BASELINE
+
+        it_s, setup_s = cpu_full_shape_iteration(args.case)
+        full = BASELINE[args.case]
+        iters = FULL_SHAPE_ITERS.get(args.case)
+        line["cpu_full_shape_s_per_iter"] = round(it_s, 2)
+        line["cpu_full_shape"] = {
+            "workload": args.case, "unknowns": full.N, "setup_s": round(setup_s, 2),
+            "s_per_iteration": round(it_s, 2),
+            "what": "one outer FGMRES iteration (preconditioner recursion, matvec, MGS) of the "
+                    "CPU oracle on the workload's own 255^2 x 4096 inputs, timed on this host",
+            "extrapolated_solve_s": round(it_s * iters, 1) if iters else None,
+            "extrapolated_unknowns_per_s": round(full.N / (it_s * iters), 1) if iters else None,
+            "extrapolation": (f"EXTRAPOLATED, not measured: x {iters} iterations (the live "
+                              f"reference's count on this workload, tests/golden/); later "
+                              f"iterations cost more (MGS grows with j), so this flatters "
+                              f"the CPU") if iters else None,
+        }
     print(json.dumps(line), flush=True)
+
+
+# outer iterations of the live reference on the full-shape workloads
+# (tests/golden/make_c5c_reference.py fingerprint)
+FULL_SHAPE_ITERS = {"c5_c": 19}
 
 
 def run_ours(args):
@@ -232,6 +278,10 @@ def run_ours(args):
     ms_per_step = ms / args.steps
     value = case.N * args.steps * world / (ms / 1000.0)
 
+    # ----- plain space-time matvec (K-MV, BASELINE's second metric): 16 B per
+    # unknown (read v, write out; the k-1 slice comes from shared memory)
+    mv = matvec_roofline(hier, case, args.steps) if rank == 0 else None
+
     # ----- e2e: public API, host buffers, H2D + setup + solve + D2H per step
     pin_u0 = torch.from_numpy(case.u0_vector()).pin_memory()
     pin_x = torch.empty(case.N, dtype=torch.float64).pin_memory()
@@ -293,6 +343,10 @@ def run_ours(args):
                 "timing": "CUDA events around every launch on its stream, over a second "
                           "pass of the same K steps right after the timed region"}
 
+    extra = None
+    if rank == 0 and world == 1 and not args.no_extra:
+        extra = extra_workloads()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v, dt, info, c = cpu_sample_solve()
@@ -320,7 +374,9 @@ def run_ours(args):
                     "includes": "H2D of u0 from pinned memory, hierarchy setup, solve, "
                                 "D2H of x into pinned memory"},
             "roofline": roof,
+            "roofline_matvec": mv,
             "cpu_baseline": cpu,
+            "extra_workloads": extra,
             "gpu_launches": launches,
             "clocks": clocks,
             "kernels": table,
@@ -328,6 +384,97 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def matvec_roofline(hier, case, steps: int):
+    """K-MV alone on the fine level (pmk_stmv, the reference's
+    BlockBidiagonalSystem.matvec): CUDA events on the launch stream around
+    `reps` launches; achieved = 16 B x unknowns / mean launch time."""
+    import torch
+
+    from paper_2401_00228_b200 import _lib
+
+    peak, peak_kind = peaks()
+    fine = hier.fine
+    v = torch.randn(case.N, dtype=torch.float64, device="cuda")
+    out = torch.empty_like(v)
+    reps = max(steps, 5)
+    fine.matvec_into(v, out)  # warm-up
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fine.matvec_into(v, out)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps / 1000.0
+    achieved = 16.0 * case.N / t / 1e9
+    del v, out
+    return {"kernel": "march_tma<MV> (pmk_stmv)", "bound": "hbm", "achieved": round(achieved, 1),
+            "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+            "bytes_per_launch": 16.0 * case.N, "ms_per_launch": round(t * 1000.0, 4),
+            "launches": reps, "peak_source": peak_kind,
+            "timing": "CUDA events on the launch stream around back-to-back launches "
+                      "(2.13 GB in, 2.13 GB out: larger than L2)"}
+
+
+# Other BASELINE shapes, device-resident, CUDA events: the "_c" companions
+# to 1e-8 (c1_c-c3_c), c4's companion (TS x TS nu = 4, theta = 1; the
+# reference needs > 200 iterations there) and literal c5 (C = 48, stagnant)
+# at a fixed budget, and c5_c_dec: BASELINE config 5's literal solver
+# structure (n_cgs = 256, one independent solve per coarse slice, FGMRES(30))
+# at the paper's Courant number, to 1e-8.
+EXTRA = [("c1_c", None), ("c2_c", None), ("c3_c", None), ("c4_c", 40), ("c5", 30),
+         ("c5_c_dec", None)]
+
+
+def extra_workloads():
+    import torch
+
+    from paper_2401_00228_b200 import multilevel_solve
+    from tests.cases import BASELINE, gpu_hierarchy
+
+    out = {}
+    for name, budget in EXTRA:
+        case = BASELINE[name] if budget is None else BASELINE[name].scaled(max_outer=budget)
+        try:
+            u0 = torch.from_numpy(case.u0_vector()).cuda()
+            h = gpu_hierarchy(case, u0=u0)
+            reps = 1 if case.N > 1e8 else 3
+            x, rep = multilevel_solve(h)  # warm-up (graph capture, tables)
+            del x
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                x, rep = multilevel_solve(h)
+                del x
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            out[name] = {
+                "unknowns": case.N, "grid": f"{case.nx}x{case.ny}", "n_t": case.n_t,
+                "theta": case.theta, "levels": case.n_levels, "schedule": list(case.schedule),
+                "nu": case.nu, "courant": case.courant, "T": case.T,
+                "coarsest_n_cgs": case.n_cgs, "restart": case.restart,
+                "budget": budget, "ms_per_solve": round(ms, 3),
+                "iterations": rep.outer_iterations,
+                "converged": bool(rep.converged),
+                "true_relative_residual": rep.metadata["true_relative_residual"],
+                "restart_cycles": rep.metadata.get("restart_cycles"),
+                ("unknowns_per_s" if budget is None else "unknown_iterations_per_s"):
+                    (case.N / (ms / 1000.0) if budget is None
+                     else case.N * rep.outer_iterations / (ms / 1000.0)),
+            }
+            del h
+        except Exception as exc:  # reported, never silently dropped
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        torch.cuda.synchronize()
+        gc.collect()
+        torch.cuda.empty_cache()
+    return out
 
 
 def main():

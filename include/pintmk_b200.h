@@ -186,6 +186,19 @@ int pmk_nrm2(const double *a, int64_t n, double *result, pmk_stream_t stream);
 int pmk_residual_nrm2(const pmk_level *L, const double *u, const double *rhs,
                       double *tmp, double *result, pmk_stream_t stream);
 
+/* Restart step of the FGMRES(m) wrapper (the
+ * reference fgmres has no restart, solver.py:366-367, so this replaces the
+ * wrapper's `r = b - hier.fine.matvec(x)` and `np.linalg.norm(r)`):
+ * r = rhs - A u stored, *result = ||r||_2 (device scalar).  r may not alias
+ * u or rhs. */
+int pmk_residual(const pmk_level *L, const double *u, const double *rhs,
+                 double *r, double *result, pmk_stream_t stream);
+
+/* y += a x (the wrapper's `x = x + dx`; a = 1 rounds once per element like
+ * numpy's addition).  x and y may not alias. */
+int pmk_axpy(double a, const double *x, double *y, int64_t n,
+             pmk_stream_t stream);
+
 /* ----------------------------------------------------- native FGMRES/MLK */
 
 typedef struct pmk_hier pmk_hier;

@@ -70,6 +70,9 @@ SIGNATURES = {
     "pmk_nrm2": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p]),
     "pmk_residual_nrm2": (c_int32, [POINTER(LevelDesc), c_void_p, c_void_p, c_void_p,
                                     c_void_p, c_void_p]),
+    "pmk_residual": (c_int32, [POINTER(LevelDesc), c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_void_p]),
+    "pmk_axpy": (c_int32, [c_double, c_void_p, c_void_p, c_int64, c_void_p]),
     "pmk_hier_create": (c_void_p, [c_int32, c_double]),
     "pmk_hier_destroy": (None, [c_void_p]),
     "pmk_hier_set_level": (c_int32, [c_void_p, c_int32, POINTER(LevelDesc),

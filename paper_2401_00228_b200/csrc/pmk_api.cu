@@ -25,9 +25,12 @@
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <unordered_map>
+#include <set>
+#include <tuple>
 #include <unordered_set>
 #include <vector>
 
@@ -95,6 +98,8 @@ Tag::~Tag() {
 
 namespace {
 
+using GraphKey = std::tuple<const double *, const int *, const double *>;
+
 struct LevelRT {
   bool set = false;
   pmk_level L{};
@@ -118,9 +123,12 @@ struct LevelRT {
   double *rhs_part = nullptr;
   int rhs_part_n = 0;
   double tol = 0.0;
-  // CUDA graphs of this level's inner solve, keyed by its output buffer
-  std::unordered_set<const double *> seen;
-  std::unordered_map<const double *, std::pair<cudaGraphExec_t, int64_t>> graphs;
+  // CUDA graphs of this level's inner solve, keyed by everything the capture
+  // bakes in that varies between calls: the output buffer, the parent's live
+  // flag and the output scale (the registered buffers and level states are
+  // fixed until drop_graphs)
+  std::set<GraphKey> seen;
+  std::map<GraphKey, std::pair<cudaGraphExec_t, int64_t>> graphs;
   bool graph_failed = false;
   // current invocation
   const double *rhs_cur = nullptr;   // rhs of this invocation (raw basis vector 0)
@@ -145,6 +153,18 @@ struct pmk_hier {
 };
 
 namespace {
+
+// Every captured graph holds device pointers of the levels below it (states,
+// registered buffers, the coarsest tables): any change to those invalidates
+// all of them.
+void drop_graphs(pmk_hier *H) {
+  for (auto &R : H->lv) {
+    for (auto &kv : R.graphs) cudaGraphExecDestroy(kv.second.first);
+    R.graphs.clear();
+    R.seen.clear();
+    R.graph_failed = false;
+  }
+}
 
 inline cudaStream_t cs(pmk_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -355,8 +375,10 @@ int fgmres_begin(pmk_hier *H, int idx, const double *rhs, int max_iter, double t
   LevelRT &R = H->lv[idx];
   PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
   PMK_RETURN_IF(!rhs || max_iter < 1, PMK_ERR_ARG);
+  const void *block = R.d_block;
   int rc = alloc_state(R, max_iter);
   if (rc) return rc;
+  if (R.d_block != block && block) drop_graphs(H);  // graphs point into the old block
   R.tol = tol;
   R.parent_live = parent_live;
   if (R.rhs_part_n > 0 && rhs == R.rhs) {
@@ -399,14 +421,15 @@ int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cud
   if (!graphs_enabled() || R.graph_failed || s == nullptr || s == cudaStreamLegacy ||
       s == cudaStreamPerThread)
     return fgmres_fixed(H, child, out, live, s, out_scale);
-  auto it = R.graphs.find(out);
+  const GraphKey key{out, live, out_scale};
+  auto it = R.graphs.find(key);
   if (it != R.graphs.end()) {
     g_launches.fetch_add(it->second.second);  // the graph's kernel nodes
     PMK_CUDA_TRY(cudaGraphLaunch(it->second.first, s));
     return 0;
   }
-  if (!R.seen.count(out)) {
-    R.seen.insert(out);
+  if (!R.seen.count(key)) {
+    R.seen.insert(key);
     return fgmres_fixed(H, child, out, live, s, out_scale);
   }
   const int64_t before = g_launches.load();
@@ -424,7 +447,7 @@ int fgmres_fixed_graph(pmk_hier *H, int child, double *out, const int *live, cud
   if (rc == 0 && e == cudaSuccess && g &&
       cudaGraphInstantiate(&exec, g, 0) == cudaSuccess) {
     cudaGraphDestroy(g);
-    R.graphs[out] = {exec, nodes};
+    R.graphs[key] = {exec, nodes};
     g_launches.fetch_add(nodes);
     PMK_CUDA_TRY(cudaGraphLaunch(exec, s));
     return 0;
@@ -903,6 +926,26 @@ int pmk_residual_nrm2(const pmk_level *L, const double *u, const double *rhs, do
   return launch_reduce_to_scalar(part, kRedBlocks, result, 1, cs(stream));
 }
 
+int pmk_residual(const pmk_level *L, const double *u, const double *rhs, double *r,
+                 double *result, pmk_stream_t stream) {
+  int rc = check_level(L);
+  if (rc) return rc;
+  PMK_RETURN_IF(!u || !rhs || !r || !result || r == u || r == rhs, PMK_ERR_ARG);
+  rc = pmk_stmv(L, u, r, stream);
+  if (rc) return rc;
+  double *part = scratch_partials();
+  PMK_RETURN_IF(!part, (int)cudaErrorMemoryAllocation);
+  rc = launch_diffsq_partials(rhs, r, level_N(*L), part, cs(stream), r);
+  if (rc) return rc;
+  return launch_reduce_to_scalar(part, kRedBlocks, result, 1, cs(stream));
+}
+
+int pmk_axpy(double a, const double *x, double *y, int64_t n, pmk_stream_t stream) {
+  PMK_RETURN_IF(!x || !y || n < 0 || x == y, PMK_ERR_ARG);
+  if (n == 0) return 0;
+  return launch_axpy(a, x, y, n, cs(stream));
+}
+
 pmk_hier *pmk_hier_create(int32_t n_levels, double mu) {
   if (n_levels < 2 || mu == 0.0) return nullptr;
   pmk_hier *H = new (std::nothrow) pmk_hier();
@@ -915,8 +958,8 @@ pmk_hier *pmk_hier_create(int32_t n_levels, double mu) {
 
 void pmk_hier_destroy(pmk_hier *H) {
   if (!H) return;
+  drop_graphs(H);
   for (auto &R : H->lv) {
-    for (auto &kv : R.graphs) cudaGraphExecDestroy(kv.second.first);
     if (R.d_block) cudaFree(R.d_block);
     if (R.rhs_part) cudaFree(R.rhs_part);
     if (R.snap) cudaFreeHost(R.snap);
@@ -932,6 +975,7 @@ int pmk_hier_set_level(pmk_hier *H, int32_t idx, const pmk_level *L, const pmk_p
   rc = check_pair(*L, P);
   if (rc) return rc;
   PMK_RETURN_IF(idx > 0 && budget < 1, PMK_ERR_ARG);
+  drop_graphs(H);
   LevelRT &R = H->lv[idx];
   R.L = *L;
   R.P = *P;
@@ -945,6 +989,7 @@ int pmk_hier_set_level(pmk_hier *H, int32_t idx, const pmk_level *L, const pmk_p
 int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C) {
   PMK_RETURN_IF(!H || !C, PMK_ERR_ARG);
   PMK_RETURN_IF(C->kind != PMK_COARSE_DST && C->kind != PMK_COARSE_DENSE, PMK_ERR_UNSUPPORTED);
+  drop_graphs(H);
   H->coarse = *C;
   H->has_coarse = true;
   return 0;
@@ -954,6 +999,7 @@ int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *v
                          double *const *child_out, int32_t n_slots, double *w_buf,
                          double *ts_scratch) {
   PMK_RETURN_IF(!H || idx < 0 || idx >= H->n_levels || !rhs, PMK_ERR_ARG);
+  drop_graphs(H);
   if (idx == H->n_levels - 1) {
     H->coarse_rhs = rhs;
     return 0;

@@ -208,7 +208,8 @@ int launch_dot_partials(const double *a, const double *a_scale, const double *b,
                         const double *b_scale, int64_t n, double *partials,
                         const int *live, cudaStream_t s);
 int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *partials,
-                           cudaStream_t s);
+                           cudaStream_t s, double *r_out = nullptr);
+int launch_axpy(double a, const double *x, double *y, int64_t n, cudaStream_t s);
 int launch_div_check(const double *x, double d, int64_t n, double *out, cudaStream_t s);
 int launch_reduce_to_scalar(const double *partials, int n, double *out, int do_sqrt,
                             cudaStream_t s);

@@ -78,11 +78,13 @@ __global__ void __launch_bounds__(kRedThreads)
 
 // partial sums of (a - b)^2 with r = a - b rounded first (stepper.py:192-193)
 __global__ void __launch_bounds__(kRedThreads)
-    diffsq_partials_kernel(const double *a, const double *b, int64_t n, double *partials) {
+    diffsq_partials_kernel(const double *a, const double *b, int64_t n, double *partials,
+                           double *r_out) {
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const double r = __dsub_rn(a[i], b[i]);
+    if (r_out) r_out[i] = r;  // (may alias b: each element is read before it is written)
     acc = __dadd_rn(acc, __dmul_rn(r, r));
   }
   const double s = block_sum(acc);
@@ -850,9 +852,25 @@ int launch_dot_partials(const double *a, const double *a_scale, const double *b,
 }
 
 int launch_diffsq_partials(const double *a, const double *b, int64_t n, double *partials,
-                           cudaStream_t s) {
-  prof::Scope scope(prof::kRed, 16.0 * (double)n, 0.0, s);
-  diffsq_partials_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, partials);
+                           cudaStream_t s, double *r_out) {
+  prof::Scope scope(prof::kRed, (r_out ? 24.0 : 16.0) * (double)n, 0.0, s);
+  diffsq_partials_kernel<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, partials, r_out);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
+// y += a x (the restart update x <- x + dx of the FGMRES(m) wrapper, SURVEY
+// section 8(c)); one rounding per element, as numpy's x + dx.
+__global__ void __launch_bounds__(256)
+    axpy_kernel(double a, const double *__restrict__ x, double *__restrict__ y, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (a == 1.0) ? __dadd_rn(y[i], x[i]) : fma(a, x[i], y[i]);
+}
+
+int launch_axpy(double a, const double *x, double *y, int64_t n, cudaStream_t s) {
+  prof::Scope scope(prof::kAsm, 24.0 * (double)n, 0.0, s);
+  axpy_kernel<<<grid_for(n, 256), 256, 0, s>>>(a, x, y, n);
   PMK_LAUNCH_CHECK();
   return 0;
 }

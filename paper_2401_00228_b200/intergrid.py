@@ -187,6 +187,10 @@ class MgritPair(_PairBase):
             from .spatial import dst_eigenvalues_1d, dst_matrix, fft_dst_tables
 
             sp_op, cfg = self.ops.spatial, self.ops.config
+            if self.ops.spectral_info is None:
+                # ideal interpolation runs in the sine basis of the fine grid
+                raise NotImplementedError(
+                    "MGRIT ideal interpolation needs build_laplacian's operator")
             nx, ny = sp_op.n_x, (sp_op.n_y if sp_op.dim == 2 else 1)
             ex = dst_eigenvalues_1d(nx)
             lam = ex[None, :] if ny == 1 else (dst_eigenvalues_1d(ny)[:, None] + ex[None, :])
@@ -242,10 +246,12 @@ def rediscretized_coarse(ops: StepOperators, nu: int, n_T: int) -> CoarseSystem:
     diag = (eye - cfg.theta * big_dt * ops.spatial.matrix).tocsr()
     sub = (eye + (1 - cfg.theta) * big_dt * ops.spatial.matrix).tocsr()
     sp_op = ops.spatial
+    spectral = None
+    if ops.spectral_info is not None:  # build_laplacian's operator
+        spectral = SpectralInfo(sp_op.tau / sp_op.delta_x**2, cfg.theta * big_dt,
+                                (1 - cfg.theta) * big_dt)
     return CoarseSystem(diag=diag, sub=sub, n_steps=n_T, provenance="rediscretized",
-                        grid=sp_op.grid, dim=sp_op.dim,
-                        spectral=SpectralInfo(sp_op.tau / sp_op.delta_x**2, cfg.theta * big_dt,
-                                              (1 - cfg.theta) * big_dt))
+                        grid=sp_op.grid, dim=sp_op.dim, spectral=spectral)
 
 
 def build_t_pair(n: int, nu: int, n_T: int) -> TimePair:

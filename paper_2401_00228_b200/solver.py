@@ -231,10 +231,11 @@ def _space_move(level: Level, time_nu: int = 1) -> Level:
 def _fine_level(fine: FineSystem) -> Level:
     ops = fine.ops
     sp_op = ops.spatial
+    pristine = ops.spectral_info is not None
     return Level(system=fine, spatial_matrix=sp_op.matrix, dt=ops.config.delta_t,
                  implicit_weight=ops.config.theta, n_steps=fine.n_t,
                  grid=(sp_op.n_x, sp_op.n_y), dim=sp_op.dim, kind="fine",
-                 laplace_factor=sp_op.tau / sp_op.delta_x**2)
+                 laplace_factor=sp_op.tau / sp_op.delta_x**2 if pristine else None)
 
 
 def time_move_is_stable(level: Level, nu: int = 2) -> bool:
@@ -469,7 +470,10 @@ def fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_ite
     restarts (reference solver.py:362-456).  tol=None runs exactly max_iter
     iterations (inner solves) unless the basis breaks down."""
     with hier.on_stream():
-        return _fgmres(hier, level_idx, rhs, tol, max_iter, keep_basis)
+        x, report = _fgmres(hier, level_idx, rhs, tol, max_iter, keep_basis)
+    if not hasattr(rhs, "data_ptr"):  # numpy in -> numpy out, like the reference
+        return x.cpu().numpy(), report
+    return x, report
 
 
 def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_iter: int,
@@ -645,8 +649,10 @@ def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart:
     import torch
 
     fine = hier.fine
+    lib = _lib.load()
     b = fine.rhs.reshape(-1)
     beta0 = _nrm2(b)
+    rn_dev = _empty(1)
     x = None          # x = 0 until the first cycle returns
     r = b
     rn = beta0
@@ -669,17 +675,20 @@ def _restarted_fgmres(hier: LevelHierarchy, tol: float, max_outer: int, restart:
         else:
             if copier is not None:
                 copier.fence()
-            x.add_(dx)
+            _lib.check(lib.pmk_axpy(1.0, _lib.ptr(dx), _lib.ptr(x), x.numel(),
+                                    _lib.stream_ptr()), "axpy")     # x = x + dx
             if copier is not None:
                 copier.start(x)
         del dx
         total += rep.outer_iterations
         cycles += 1
         hist += [h * rn / beta0 for h in rep.residual_history]
-        r = torch.empty_like(b)
-        fine.matvec_into(x, r)
-        torch.sub(b, r, out=r)     # r = b - A x
-        rn = _nrm2(r)
+        if r is b:
+            r = _empty(b.numel())
+        _lib.check(lib.pmk_residual(ctypes.byref(fine.level_desc()), _lib.ptr(x), _lib.ptr(b),
+                                    _lib.ptr(r), _lib.ptr(rn_dev), _lib.stream_ptr()),
+                   "residual")          # r = b - A x, ||r||
+        rn = float(rn_dev.item())
         final_rel = rn / beta0     # ||b - A x|| / ||b|| (stepper.py:191-193)
         if final_rel <= tol:
             converged = True

@@ -14,7 +14,7 @@ included), so code written against the reference keeps working.
 from __future__ import annotations
 
 import ctypes
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import scipy.sparse as sp
@@ -57,11 +57,8 @@ class _LazyDiagSolve:
         """Solve psi x = rhs for one vector or a (k, n) block of row vectors."""
         if self._sys is None:
             o = self._ops
-            self._sys = BlockBidiagonalSystem(
-                o.psi, o.phi, 0, grid=o.spatial.grid, dim=o.spatial.dim,
-                spectral=SpectralInfo(o.spatial.tau / o.spatial.delta_x**2,
-                                      o.config.theta * o.config.delta_t,
-                                      (1.0 - o.config.theta) * o.config.delta_t))
+            self._sys = BlockBidiagonalSystem(o.psi, o.phi, 0, grid=o.spatial.grid,
+                                              dim=o.spatial.dim, spectral=o.spectral_info)
         return self._sys.diag_solve(rhs)
 
 
@@ -74,14 +71,44 @@ class StepOperators:
     psi_factorization: object
     spatial: SpatialOperator
     config: ThetaSchemeConfig
+    _spectral: object = field(default=None, init=False, repr=False)
+    _spectral_known: bool = field(default=False, init=False, repr=False)
 
     @property
     def n(self) -> int:
         return self.phi.shape[0]
 
+    @property
+    def spectral_info(self) -> SpectralInfo | None:
+        """SpectralInfo when psi/phi are the theta-scheme blocks of
+        build_laplacian's operator (the device then takes closed-form stencils
+        and the sine-basis coarse solve), else None: the kernels read the
+        actual matrices (checked once, O(nnz) compares)."""
+        if not self._spectral_known:
+            spec = None
+            op, cfg = self.spatial, self.config
+            if _is_pristine(op):
+                cand = SpectralInfo(op.tau / op.delta_x**2, cfg.theta * cfg.delta_t,
+                                    (1.0 - cfg.theta) * cfg.delta_t)
+                d, b = cand.stencils(op.dim)
+                if _csr_equal(self.psi, stencil_csr(op.n_x, op.n_y, d)) and \
+                        _csr_equal(self.phi, stencil_csr(op.n_x, op.n_y, b)):
+                    spec = cand
+            self._spectral = spec
+            self._spectral_known = True
+        return self._spectral
+
+
+def _csr_equal(a, b) -> bool:
+    a = sp.csr_matrix(a)
+    a.sort_indices()
+    return (a.shape == b.shape and a.nnz == b.nnz and np.array_equal(a.indptr, b.indptr)
+            and np.array_equal(a.indices, b.indices) and np.array_equal(a.data, b.data))
+
 
 def build_step_operators(op: SpatialOperator, cfg: ThetaSchemeConfig) -> StepOperators:
     """phi = I + (1-theta) dt A, psi = I - theta dt A (reference stepper.py:56-63)."""
+    spec = None
     if _is_pristine(op):
         # closed form, entry for entry scipy's eye -/+ s * A
         # (tests/test_host.py::test_direct_csr_assembly_bitwise)
@@ -95,6 +122,8 @@ def build_step_operators(op: SpatialOperator, cfg: ThetaSchemeConfig) -> StepOpe
         phi = (eye + (1.0 - cfg.theta) * cfg.delta_t * op.matrix).tocsr()
         psi = (eye - cfg.theta * cfg.delta_t * op.matrix).tocsr()
     ops = StepOperators(phi=phi, psi=psi, psi_factorization=None, spatial=op, config=cfg)
+    ops._spectral = spec   # (known: built right here)
+    ops._spectral_known = True
     ops.psi_factorization = _LazyDiagSolve(ops)
     return ops
 
@@ -302,11 +331,10 @@ class FineSystem(BlockBidiagonalSystem):
         if forcing is not None and tuple(forcing.shape) != (ops.config.n_t, ops.n):
             raise ValueError("forcing must have shape (n_t, n)")
         sp_op = ops.spatial
+        # spectral only for build_laplacian's operator (otherwise the kernels
+        # read psi/phi themselves and the coarse solve takes the general path)
         super().__init__(diag=ops.psi, sub=ops.phi, n_steps=ops.config.n_t,
-                         grid=sp_op.grid, dim=sp_op.dim,
-                         spectral=SpectralInfo(sp_op.tau / sp_op.delta_x**2,
-                                               ops.config.theta * ops.config.delta_t,
-                                               (1.0 - ops.config.theta) * ops.config.delta_t))
+                         grid=sp_op.grid, dim=sp_op.dim, spectral=ops.spectral_info)
         torch = _lib.require_cuda()
         self.ops = ops
         self.host_io = not isinstance(u0, torch.Tensor)
