@@ -43,7 +43,7 @@ enum {
 };
 
 /* Coarsest-level direct solver kinds (pmk_coarse.kind). */
-enum { PMK_COARSE_DST = 1, PMK_COARSE_DENSE = 2 };
+enum { PMK_COARSE_DST = 1, PMK_COARSE_DENSE = 2, PMK_COARSE_EIG = 3 };
 
 /*
  * Spatial operator in "right-product" form: (v @ M)_i = sum_j M[j,i] v_j,
@@ -114,8 +114,19 @@ typedef struct pmk_pair {
  *      (pristine Dirichlet Laplacian levels); delta/beta are their
  *      eigenvalues per mode (p fastest).  One launch chain: x-transform,
  *      y-transform, segmented per-mode recurrence, inverse transforms.
- * DENSE: explicit D^{-1} (m x m, row-major) for agglomerated levels whose
- *      operator is not Toeplitz (intergrid.py:202-227 odd-grid groups).
+ * EIG: D = I - K and B = I + b K with K = I (x) Kx + Ky (x) I, Kx, Ky
+ *      tridiagonal (every agglomerated level: intergrid.py:202-227 groups are
+ *      a tensor product; the odd-grid 3-wide last group makes K
+ *      non-symmetric).  V = Vy (x) Vx (eigenvectors of K) diagonalises D and
+ *      B: dense transforms as fp64 GEMMs over all slices (sx = Vx^{-T} and
+ *      ix = Vx^T right operands, sy = Vy^{-1} and iy = Vy left operands),
+ *      the per-mode recurrence, and in 2-D (B^T coupling) a low-rank mode
+ *      coupling b V^{-1} (K^T - K) V applied by a cluster-per-chain kernel:
+ *      n_cx points with rows cx_h [n_cx][nx] (physical extraction) and
+ *      cx_u [n_cx][nx] (mode injection), likewise cy_* along y.  Chains
+ *      start at seg_start[0..n_seg) (rows; the first is 1).
+ * DENSE: explicit D^{-1} (m x m, row-major) for 5-point operators that are
+ *      not separable (m <= 8192).
  */
 typedef struct pmk_coarse {
   int32_t kind;
@@ -136,6 +147,13 @@ typedef struct pmk_coarse {
    * 2/N_x in 1-D) folds the orthonormalisation into the recurrence. */
   const double *fft_x, *fft_y;
   double fft_scale;
+  /* EIG (and the DST GEMM path): inverse transforms; NULL = sx / sy */
+  const double *ix, *iy;
+  int32_t n_cx, n_cy; /* EIG 2-D coupling correction points (<= 8 each) */
+  const double *cx_h, *cx_u, *cy_h, *cy_u;
+  double coupling_b;  /* b in B = I + b K */
+  const int32_t *seg_start; /* device [n_seg] first row of each chain */
+  int32_t n_seg;
 } pmk_coarse;
 
 /* ---------------------------------------------------------------- per-op */

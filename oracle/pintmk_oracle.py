@@ -403,9 +403,12 @@ def build_mgrit(dim, nx, ny, theta, dt, n_t, u0, cfg: Config, nu=2, tau=1.0,
 
 
 def build(dim, nx, ny, theta, dt, n_t, u0, n_levels, schedule, cfg: Config, nu=2,
-          tau=1.0, length=1.0, forcing=None) -> Hierarchy:
-    """FineSystem (stepper.py:168-185) + build_hierarchy (solver.py:178-216)."""
-    a, _dx = laplacian(dim, nx, ny, tau, length)
+          tau=1.0, length=1.0, forcing=None, a=None) -> Hierarchy:
+    """FineSystem (stepper.py:168-185) + build_hierarchy (solver.py:178-216).
+    `a`: a caller's spatial matrix instead of build_laplacian's (the
+    reference accepts any SpatialOperator, spatial.py:17-34)."""
+    if a is None:
+        a, _dx = laplacian(dim, nx, ny, tau, length)
     d, b = blocks_from(a, theta, dt)
     fine = System(d, b, n_t)
     rhs = np.zeros((n_t + 1, a.shape[0]))

@@ -230,6 +230,124 @@ class SpectralInfo:
                 np.array([0.0, s_off, s_c, s_off, 0.0]))
 
 
+def _tridiag_eig(lower: np.ndarray, diag: np.ndarray, upper: np.ndarray):
+    """Eigen-decomposition K = V diag(lam) V^{-1} of a real tridiagonal K
+    (lower[i] = K[i, i-1], upper[i] = K[i, i+1]) whose off-diagonal products
+    are positive: K = Dl T Dl^{-1} with T symmetric (Dl diagonal), so
+    V = Dl Q and V^{-1} = Q^T Dl^{-1}.  None when some product is <= 0."""
+    from scipy.linalg import eigh_tridiagonal
+
+    n = diag.size
+    if n == 1:
+        return np.ones((1, 1)), np.ones((1, 1)), diag.copy()
+    prod = lower[1:] * upper[:-1]
+    if np.any(prod <= 0.0):
+        return None
+    # Dl[i+1] / Dl[i] = sqrt(lower[i+1] / upper[i]); log-space for range
+    ratio = 0.5 * (np.log(np.abs(lower[1:])) - np.log(np.abs(upper[:-1])))
+    logd = np.concatenate([[0.0], np.cumsum(ratio)])
+    logd -= 0.5 * (logd.max() + logd.min())
+    dl = np.exp(logd)
+    off = np.sign(upper[:-1]) * np.sqrt(prod)
+    lam, q = eigh_tridiagonal(diag, off)
+    v = dl[:, None] * q
+    vinv = q.T / dl[None, :]
+    return v, vinv, lam
+
+
+class SeparableFactors:
+    """D = I - K, B = I + b K with K = I (x) Kx + Ky (x) I (x fastest) and
+    tridiagonal Kx, Ky: true for every level this package builds (pristine
+    Laplacian levels, and agglomerated ones, since agglomerate_partition is
+    a tensor product of 1-D groupings, intergrid.py:202-227) and checked
+    here on the matrices themselves.  K's eigenvectors V = Vy (x) Vx
+    diagonalise D and B together; in 2-D the reference couples slices with
+    B^T (stepper.py:144), which differs from B by b N, N = K^T - K, when
+    agglomeration left K non-symmetric (odd grids: the 3-wide last group).
+    N is a handful of entries next to the odd group, so in the mode basis it
+    is a low-rank correction: per direction, `points` physical indices c with
+    h_c = row c of V (the physical value at c of a mode row) and
+    u_c = sum over N's entries (r, c, val) of val * column r of V^{-1}."""
+
+    MAX_POINTS = 8
+
+    def __init__(self, vx, vxi, lx, vy, vyi, ly, b, corr_x, corr_y):
+        self.vx, self.vxi, self.lx = vx, vxi, lx
+        self.vy, self.vyi, self.ly = vy, vyi, ly
+        self.b = b
+        self.corr_x, self.corr_y = corr_x, corr_y  # (h [P][n], u [P][n]) or None
+
+    @staticmethod
+    def _correction(lower, upper, v, vinv):
+        s = lower[1:] - upper[:-1]          # N[i, i+1] = K[i+1, i] - K[i, i+1]
+        idx = np.flatnonzero(s != 0.0)
+        if idx.size == 0:
+            return None
+        cols: dict = {}
+        for i in idx:                        # entries (i, i+1, s_i), (i+1, i, -s_i)
+            cols.setdefault(i + 1, []).append((i, s[i]))
+            cols.setdefault(i, []).append((i + 1, -s[i]))
+        if len(cols) > SeparableFactors.MAX_POINTS:
+            return False
+        pts = sorted(cols)
+        h = np.stack([v[c, :] for c in pts])
+        u = np.stack([sum(val * vinv[:, r] for r, val in cols[c]) for c in pts])
+        return np.ascontiguousarray(h), np.ascontiguousarray(u)
+
+    @classmethod
+    def detect(cls, diag, sub, nx: int, ny: int, dim: int, tol: float = 1e-12):
+        m = nx * ny
+        d = sp.csr_matrix(diag)
+        b = sp.csr_matrix(sub)
+        eye = sp.identity(m, format="csr")
+        try:
+            kt = StencilTable(eye - d, nx, ny).coef
+            et = StencilTable(b - eye, nx, ny).coef
+        except NotImplementedError:
+            return None
+        kk = float(np.sum(kt * kt))
+        if kk == 0.0:
+            return None
+        bfac = float(np.sum(kt * et)) / kk
+        scale = max(float(np.abs(et).max()), float(np.abs(kt).max()) * abs(bfac), 1e-300)
+        if float(np.abs(et - bfac * kt).max()) > tol * scale:
+            return None                      # B is not I + b K
+        S, W, C, E, N = (kt[s].reshape(ny, nx) for s in range(5))
+        kscale = float(np.abs(kt).max())
+        close = lambda a, ref: float(np.abs(a - ref).max()) <= tol * kscale  # noqa: E731
+        if not (close(W, W[:1]) and close(E, E[:1]) and close(S, S[:, :1]) and
+                close(N, N[:, :1])):
+            return None
+        c0 = C[0, 0]
+        if not close(C, C[:1, :] + C[:, :1] - c0):
+            return None
+        if dim == 1 or ny == 1:
+            fx = _tridiag_eig(W[0], C[0], E[0])
+            if fx is None:
+                return None
+            vy = vyi = np.ones((1, 1))
+            ly = np.zeros(1)
+            vx, vxi, lx = fx
+            corr_x = corr_y = None           # 1-D couples with B itself (_chain.pyx:64-71)
+        else:
+            fx = _tridiag_eig(W[0], C[0] - 0.5 * c0, E[0])
+            fy = _tridiag_eig(S[:, 0], C[:, 0] - 0.5 * c0, N[:, 0])
+            if fx is None or fy is None:
+                return None
+            vx, vxi, lx = fx
+            vy, vyi, ly = fy
+            corr_x = cls._correction(W[0], E[0], vx, vxi)
+            corr_y = cls._correction(S[:, 0], N[:, 0], vy, vyi)
+            if corr_x is False or corr_y is False:
+                return None
+        return cls(vx, vxi, lx, vy, vyi, ly, bfac, corr_x, corr_y)
+
+    def mode_tables(self):
+        """(delta, beta) per mode, y-mode slow: eigenvalues of D and B."""
+        lam = (self.ly[:, None] + self.lx[None, :]).ravel()
+        return 1.0 - lam, 1.0 + self.b * lam
+
+
 class CoarseSolver:
     """Device tables of the block forward substitution of one level
     (reference stepper.py:114-146)."""
@@ -243,6 +361,7 @@ class CoarseSolver:
         self.n_steps = n_steps
         self.N = (n_steps + 1) * self.m
         mask = dropped_mask(n_steps, dropped)
+        self._dropped = tuple(dropped)
         self._mask = None if mask is None else torch.from_numpy(mask).cuda()
         self._keep = []
         d = _lib.CoarseDesc()
@@ -291,11 +410,15 @@ class CoarseSolver:
             # 2-D: second transform buffer; 1-D: chunked-recurrence scratch
             self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
             self.kind = "dst"
+        elif (fac := SeparableFactors.detect(diag, sub, self.nx, self.ny, dim)) is not None \
+                and (self.nx <= 8192 if self.ny == 1 else (self.nx <= 256 and self.ny <= 512)):
+            self._setup_eig(d, fac, torch)
         else:
             if self.m > DENSE_MAX_M:
                 raise NotImplementedError(
-                    f"coarsest level with {self.m} non-Toeplitz unknowns per slice exceeds the "
-                    f"dense-inverse limit ({DENSE_MAX_M}); coarsen further")
+                    f"coarsest level with {self.m} unknowns per slice whose operator is neither "
+                    f"separable nor a sine-diagonal Laplacian exceeds the dense-inverse limit "
+                    f"({DENSE_MAX_M})")
             d.kind = _lib.PMK_COARSE_DENSE
             dd = np.asarray(sp.csr_matrix(diag).toarray())
             try:
@@ -316,6 +439,51 @@ class CoarseSolver:
         d.work0 = self.work0.data_ptr()
         d.work1 = None if self.work1 is None else self.work1.data_ptr()
         self.desc = d
+
+    def _setup_eig(self, d, fac: "SeparableFactors", torch) -> None:
+        """EIG tables: dense eigen-transforms (GEMM operands), per-mode
+        eigenvalues of D and B, the 2-D low-rank B^T correction and the chain
+        starts (reference segment_rows, stepper.py:107-112)."""
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+        d.kind = _lib.PMK_COARSE_EIG
+        keep = []
+
+        def put(name, arr):
+            t = dev(arr)
+            keep.append(t)
+            setattr(d, name, t.data_ptr())
+
+        put("sx", fac.vxi.T)   # forward x: rows times Vx^{-T}
+        put("ix", fac.vx.T)    # inverse x: rows times Vx^T
+        if self.ny > 1:
+            put("sy", fac.vyi)  # forward y: Vy^{-1} times the slice
+            put("iy", fac.vy)
+        delta, beta = fac.mode_tables()
+        put("delta", delta)
+        put("beta", beta)
+        d.coupling_b = fac.b
+        d.n_cx = d.n_cy = 0
+        if self.ny > 1 and fac.corr_x is not None:
+            d.n_cx = fac.corr_x[0].shape[0]
+            put("cx_h", fac.corr_x[0])
+            put("cx_u", fac.corr_x[1])
+        if self.ny > 1 and fac.corr_y is not None:
+            d.n_cy = fac.corr_y[0].shape[0]
+            put("cy_h", fac.corr_y[0])
+            put("cy_u", fac.corr_y[1])
+        cuts = sorted(int(c) for c in self._dropped if c > 1)
+        starts = np.array([1] + cuts, dtype=np.int32) if self.n_steps >= 1 else \
+            np.array([1], dtype=np.int32)
+        st = torch.from_numpy(starts).cuda()
+        keep.append(st)
+        d.seg_start = st.data_ptr()
+        d.n_seg = int(starts.size) if self.n_steps >= 1 else 0
+        self._keep += keep
+        self.factors = fac
+        self.work0 = torch.empty(self.N, dtype=torch.float64, device="cuda")
+        self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
+        self.kind = "eig"
+        self.kind_detail = "eig-chain" if (d.n_cx or d.n_cy) else "eig"
 
     def solve_into(self, rhs, out) -> None:
         lib = _lib.load()

@@ -24,6 +24,7 @@ PMK_ERR_UNSUPPORTED = 1003
 PMK_ERR_STATE = 1004
 PMK_COARSE_DST = 1
 PMK_COARSE_DENSE = 2
+PMK_COARSE_EIG = 3
 
 
 class Stencil(ctypes.Structure):
@@ -52,7 +53,10 @@ class CoarseDesc(ctypes.Structure):
                 ("sy", c_void_p), ("delta", c_void_p), ("beta", c_void_p),
                 ("dinv", c_void_p), ("coupling", Stencil), ("work0", c_void_p),
                 ("work1", c_void_p), ("fft_x", c_void_p), ("fft_y", c_void_p),
-                ("fft_scale", c_double)]
+                ("fft_scale", c_double), ("ix", c_void_p), ("iy", c_void_p),
+                ("n_cx", c_int32), ("n_cy", c_int32), ("cx_h", c_void_p), ("cx_u", c_void_p),
+                ("cy_h", c_void_p), ("cy_u", c_void_p), ("coupling_b", c_double),
+                ("seg_start", c_void_p), ("n_seg", c_int32)]
 
 
 # name -> (restype, argtypes); exactly the functions include/pintmk_b200.h declares

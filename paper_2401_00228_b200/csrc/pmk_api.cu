@@ -56,7 +56,8 @@ std::vector<cudaEvent_t> g_pool;
 size_t g_pool_used = 0;
 const char *kCatNames[prof::kNumCat] = {"march_mv", "march_mvr", "march_imv", "mgs_pass",
                                          "reduce",   "fgmres_small", "assemble", "coarse_gemm",
-                                         "coarse_recurrence", "coarse_misc", "transfer"};
+                                         "coarse_recurrence", "coarse_misc", "transfer",
+                                         "coarse_dst", "coarse_chain"};
 
 cudaEvent_t pool_event() {
   if (g_pool_used == g_pool.size()) {
@@ -988,7 +989,9 @@ int pmk_hier_set_level(pmk_hier *H, int32_t idx, const pmk_level *L, const pmk_p
 
 int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C) {
   PMK_RETURN_IF(!H || !C, PMK_ERR_ARG);
-  PMK_RETURN_IF(C->kind != PMK_COARSE_DST && C->kind != PMK_COARSE_DENSE, PMK_ERR_UNSUPPORTED);
+  PMK_RETURN_IF(C->kind != PMK_COARSE_DST && C->kind != PMK_COARSE_DENSE &&
+                    C->kind != PMK_COARSE_EIG,
+                PMK_ERR_UNSUPPORTED);
   drop_graphs(H);
   H->coarse = *C;
   H->has_coarse = true;

@@ -19,6 +19,8 @@
 //
 // This translation unit keeps FMA contraction on (DFMA GEMM); the result
 // differs from the reference's LU / Thomas solve by rounding only.
+#include <cooperative_groups.h>
+
 #include "pmk_internal.cuh"
 
 namespace pmk {
@@ -31,15 +33,19 @@ constexpr int BM = 64, BN = 64, BK = 16;
 __global__ void __launch_bounds__(256)
     dgemm_nn_kernel(int M, int N, int K, const double *__restrict__ A, int lda, int64_t sA,
                     const double *__restrict__ B, int ldb, int64_t sB, double *__restrict__ C,
-                    int ldc, int64_t sC, const int *live) {
+                    int ldc, int64_t sC, int batch, const int *live) {
   if (!is_live(live)) return;
   __shared__ double As[2][BK][BM + 1];
   __shared__ double Bs[2][BK][BN];
-  const int bz = blockIdx.z;
-  A += bz * sA;
-  B += bz * sB;
-  C += bz * sC;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int mtiles = (M + BM - 1) / BM;
+  // grid-stride over (batch, M tile): gridDim.y / .z stay within their limits
+  for (int64_t bt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y; bt < (int64_t)batch * mtiles;
+       bt += (int64_t)gridDim.z * gridDim.y) {
+  const int bz = (int)(bt / mtiles);
+  const double *__restrict__ Ab = A + bz * sA;
+  const double *__restrict__ Bb = B + bz * sB;
+  double *__restrict__ Cb = C + bz * sC;
+  const int m0 = (int)(bt % mtiles) * BM, n0 = blockIdx.x * BN;
   const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
   double acc[4][4];
 #pragma unroll
@@ -53,13 +59,13 @@ __global__ void __launch_bounds__(256)
     for (int q = 0; q < 4; ++q) {
       const int r = (t >> 4) + 16 * q, c = t & 15;
       const int gm = m0 + r, gk = k0 + c;
-      ra[q] = (gm < M && gk < K) ? A[(int64_t)gm * lda + gk] : 0.0;
+      ra[q] = (gm < M && gk < K) ? Ab[(int64_t)gm * lda + gk] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int r = (t >> 6) + 4 * q, c = t & 63;
       const int gk = k0 + r, gn = n0 + c;
-      rb[q] = (gk < K && gn < N) ? B[(int64_t)gk * ldb + gn] : 0.0;
+      rb[q] = (gk < K && gn < N) ? Bb[(int64_t)gk * ldb + gn] : 0.0;
     }
   };
   auto sstore = [&](int buf) {
@@ -98,18 +104,23 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int gn = n0 + tx + 16 * j;
-      if (gn < N) C[(int64_t)gm * ldc + gn] = acc[i][j];
+      if (gn < N) Cb[(int64_t)gm * ldc + gn] = acc[i][j];
     }
+  }
+  __syncthreads();  // (shared tiles are reused by the next (batch, tile))
   }
 }
 
 int gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B, int ldb,
          int64_t sB, double *C, int ldc, int64_t sC, int batch, const int *live, cudaStream_t s) {
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, batch);
+  const int mtiles = (M + BM - 1) / BM;
+  const int gy = mtiles < 4096 ? mtiles : 4096;
+  const int gz = batch < 1024 ? batch : 1024;
+  dim3 grid((N + BN - 1) / BN, gy, gz);
   const double flops = 2.0 * M * N * (double)K * batch;
   const double bytes = 8.0 * batch * ((double)M * N * 2.0) + 8.0 * (double)K * N;
   prof::Scope scope(prof::kGemm, bytes, flops, s);
-  dgemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, live);
+  dgemm_nn_kernel<<<grid, 256, 0, s>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, live);
   PMK_LAUNCH_CHECK();
   return 0;
 }
@@ -319,6 +330,258 @@ int strided_copy(const double *src, int64_t sstride, int64_t soff, double *dst, 
   return 0;
 }
 
+// ---------------------------------------------------------------- EIG chain
+// Mode-space block forward substitution of a 2-D EIG level whose slices are
+// coupled by B^T != B (stepper.py:144 on an agglomerated odd grid):
+//   z_k = (r_k + beta z_{k-1} + b C(z_{k-1})) / delta,   C = I (x) Cx + Cy (x) I,
+//   Cx z_row = sum_c u_c (h_c . z_row)   (points c of K^T - K, see pmk_coarse),
+// in place on X ((n_steps+1) x ny x nx modes, y-mode slow).  One thread
+// cluster per chain (segment); CTA g of the cluster owns mode rows
+// [g RQ, g RQ + RQ), thread p owns mode column p, so z, 1/delta and beta of
+// its RQ modes stay in registers for the whole chain.  Per step: the row dots
+// h_c . z_row are warp-transposed sums (31 shuffles for 32 values) completed
+// across warps in shared memory; the column dots h_c . z_col are thread-local
+// over the CTA's rows, completed across the cluster through distributed
+// shared memory after one cluster barrier.  Buffers alternate by step parity,
+// so that barrier is the only cluster-wide synchronisation per step.
+struct EigChainArgs {
+  double *X;
+  const double *delta, *beta;
+  const uint8_t *dropped;
+  const int32_t *seg_start;
+  int n_seg, n_steps, nx, ny, n_cx, n_cy;
+  const double *cx_h, *cx_u, *cy_h, *cy_u;
+  double b;
+  const int *live;
+};
+
+// v[i] over the 32 lanes -> lane l returns sum_lanes v[l] (fixed order)
+template <int NV>
+__device__ __forceinline__ double warp_transpose_sum(double (&v)[NV], int base) {
+  static_assert(NV % 32 == 0, "");
+  double w[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) w[i] = v[base + i];
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int i = 0; i < o; ++i) {
+      const double send = up ? w[i] : w[i + o];
+      const double keep = up ? w[i + o] : w[i];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  return w[0];
+}
+
+template <int RQ, int NC>
+__global__ void __launch_bounds__(256) eig_chain_kernel(EigChainArgs a) {
+  namespace cg = cooperative_groups;
+  if (!is_live(a.live)) return;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int G = (int)cluster.num_blocks();
+  const int g = (int)cluster.block_rank();
+  const int seg = blockIdx.x / G;
+  if (seg >= a.n_seg) return;  // (whole clusters only: uniform)
+  const int nx = a.nx, ny = a.ny;
+  const int64_t m = (int64_t)nx * ny;
+  const int p = threadIdx.x;
+  const bool colok = p < nx;
+  const int NT = blockDim.x, NW = NT >> 5, warp = p >> 5, lane = p & 31;
+  const int q0 = g * RQ;
+  constexpr int NV = ((RQ * NC + 31) / 32) * 32;
+  extern __shared__ double sm[];
+  double *cxh = sm;                       // [NC][nx]
+  double *cxu = cxh + NC * nx;            // [NC][nx]
+  double *cyh = cxu + NC * nx;            // [NC][ny]
+  double *cyu = cyh + NC * ny;            // [NC][ny]
+  double *dpart = cyu + NC * ny;          // [2][NW][NV]
+  double *dsum = dpart + 2 * NW * NV;     // [2][NV]
+  double *epart = dsum + 2 * NV;          // [2][NC][NT]  (read by the cluster)
+  for (int i = threadIdx.x; i < NC * nx; i += NT) {
+    const int c = i / nx, x = i - c * nx;
+    cxh[i] = c < a.n_cx ? a.cx_h[(int64_t)c * nx + x] : 0.0;
+    cxu[i] = c < a.n_cx ? a.cx_u[(int64_t)c * nx + x] : 0.0;
+  }
+  for (int i = threadIdx.x; i < NC * ny; i += NT) {
+    const int c = i / ny, y = i - c * ny;
+    cyh[i] = c < a.n_cy ? a.cy_h[(int64_t)c * ny + y] : 0.0;
+    cyu[i] = c < a.n_cy ? a.cy_u[(int64_t)c * ny + y] : 0.0;
+  }
+  double invd[RQ], bt[RQ], z[RQ], r[RQ];
+#pragma unroll
+  for (int q = 0; q < RQ; ++q) {
+    const int y = q0 + q;
+    const bool ok = colok && y < ny;
+    const int64_t i = (int64_t)y * nx + p;
+    invd[q] = ok ? 1.0 / a.delta[i] : 0.0;
+    bt[q] = ok ? a.beta[i] : 0.0;
+  }
+  const int k0 = a.seg_start[seg];
+  const int k1 = (seg + 1 < a.n_seg) ? a.seg_start[seg + 1] : a.n_steps + 1;
+  auto load_rows = [&](int k, double (&dst)[RQ]) {
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      const int y = q0 + q;
+      dst[q] = (colok && y < ny) ? a.X[(int64_t)k * m + (int64_t)y * nx + p] : 0.0;
+    }
+  };
+  load_rows(k0 - 1, z);  // previous slice (used only when k0 is not a cut)
+  load_rows(k0, r);
+  __syncthreads();
+  double hx[NC], ux[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    hx[c] = colok ? cxh[c * nx + p] : 0.0;
+    ux[c] = colok ? cxu[c * nx + p] : 0.0;
+  }
+  for (int k = k0; k < k1; ++k) {
+    double rn[RQ];
+    if (k + 1 < k1) load_rows(k + 1, rn);
+    const bool cut = (k == k0) && a.dropped && a.dropped[k];
+    if (cut) {
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) z[q] = r[q] * invd[q];
+    } else {
+      const int buf = k & 1;
+      // row dots: value j = q * NC + c
+      double v[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) v[j] = 0.0;
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) v[q * NC + c] = hx[c] * z[q];
+#pragma unroll
+      for (int b0 = 0; b0 < NV; b0 += 32) {
+        const double sum = warp_transpose_sum<NV>(v, b0);
+        dpart[(buf * NW + warp) * NV + b0 + lane] = sum;
+      }
+      // column partials over this CTA's rows
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        double e = 0.0;
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const int y = q0 + q;
+          if (y < ny) e = fma(cyh[c * ny + y], z[q], e);
+        }
+        epart[(buf * NC + c) * NT + p] = e;
+      }
+      cluster.sync();  // dpart (CTA) and epart (cluster) complete
+      for (int j = threadIdx.x; j < NV; j += NT) {
+        double sacc = 0.0;
+        for (int w = 0; w < NW; ++w) sacc += dpart[(buf * NW + w) * NV + j];
+        dsum[buf * NV + j] = sacc;
+      }
+      double e[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) e[c] = 0.0;
+      for (int gg = 0; gg < G; ++gg) {
+        const double *peer = cluster.map_shared_rank(epart, gg);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) e[c] += peer[(buf * NC + c) * NT + p];
+      }
+      __syncthreads();  // dsum
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        const int y = q0 + q;
+        double corr = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          corr = fma(ux[c], dsum[buf * NV + q * NC + c], corr);
+          if (y < ny) corr = fma(cyu[c * ny + y], e[c], corr);
+        }
+        z[q] = fma(a.b, corr, fma(bt[q], z[q], r[q])) * invd[q];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+      const int y = q0 + q;
+      if (colok && y < ny) a.X[(int64_t)k * m + (int64_t)y * nx + p] = z[q];
+    }
+    if (k + 1 < k1) {
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) r[q] = rn[q];
+    }
+  }
+  cluster.sync();  // no CTA leaves while a peer may still read its epart
+}
+
+template <int RQ, int NC>
+int launch_eig_chain_t(const EigChainArgs &a, int G, cudaStream_t s) {
+  const int NT = ((a.nx + 31) / 32) * 32;
+  const int NW = NT / 32;
+  constexpr int NV = ((RQ * NC + 31) / 32) * 32;
+  const size_t smem =
+      sizeof(double) * (2 * NC * (size_t)a.nx + 2 * NC * (size_t)a.ny + 2 * (size_t)NW * NV +
+                        2 * NV + 2 * (size_t)NC * NT);
+  auto fn = eig_chain_kernel<RQ, NC>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    PMK_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    PMK_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      227 * 1024));
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(a.n_seg * G), 1, 1);
+  cfg.blockDim = dim3((unsigned)NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PMK_CUDA_TRY(cudaLaunchKernelEx(&cfg, fn, a));
+  return 0;
+}
+
+int launch_eig_chain(const pmk_coarse &C, double *X, const int *live, cudaStream_t s) {
+  const int nx = C.nx, ny = C.ny;
+  PMK_RETURN_IF(nx > 256 || C.n_cx > 8 || C.n_cy > 8 || !C.seg_start || C.n_seg < 1,
+                PMK_ERR_UNSUPPORTED);
+  EigChainArgs a;
+  a.X = X;
+  a.delta = C.delta;
+  a.beta = C.beta;
+  a.dropped = C.dropped;
+  a.seg_start = C.seg_start;
+  a.n_seg = C.n_seg;
+  a.n_steps = C.n_steps;
+  a.nx = nx;
+  a.ny = ny;
+  a.n_cx = C.n_cx;
+  a.n_cy = C.n_cy;
+  a.cx_h = C.cx_h;
+  a.cx_u = C.cx_u;
+  a.cy_h = C.cy_h;
+  a.cy_u = C.cy_u;
+  a.b = C.coupling_b;
+  a.live = live;
+  const int nc = C.n_cx > C.n_cy ? C.n_cx : C.n_cy;
+  // rows per CTA: the smallest that keeps the cluster within 8 CTAs (16 at most)
+  int rq = 4;
+  while (rq < 32 && (ny + rq - 1) / rq > 8) rq *= 2;
+  const int G = (ny + rq - 1) / rq;
+  PMK_RETURN_IF(G > 16, PMK_ERR_UNSUPPORTED);
+  const int64_t N = (int64_t)(C.n_steps + 1) * nx * ny;
+  prof::Scope sc(prof::kChain, 16.0 * N, 0.0, s);
+#define PMK_EIG_CASE(R, NCV) \
+  if (rq == R && nc <= NCV) return launch_eig_chain_t<R, NCV>(a, G, s);
+  PMK_EIG_CASE(4, 2) PMK_EIG_CASE(4, 4) PMK_EIG_CASE(4, 8)
+  PMK_EIG_CASE(8, 2) PMK_EIG_CASE(8, 4) PMK_EIG_CASE(8, 8)
+  PMK_EIG_CASE(16, 2) PMK_EIG_CASE(16, 4)
+  PMK_EIG_CASE(32, 2)
+#undef PMK_EIG_CASE
+  return PMK_ERR_UNSUPPORTED;
+}
+
 }  // namespace
 
 // MgritPair.restrict (intergrid.py:152-155): vh[K] = v[nu K].
@@ -438,36 +701,40 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     PMK_LAUNCH_CHECK();
     return 0;
   }
-  if (C.kind == PMK_COARSE_DST) {
+  if (C.kind == PMK_COARSE_DST || C.kind == PMK_COARSE_EIG) {
+    // dense transforms as GEMMs over all slices: forward R Fx (rows), Fy R_k
+    // (per slice); inverse Iy Z_k, then Z Ix.  Sine basis: F = I = S.
     PMK_RETURN_IF(!C.sx || !C.delta || !C.beta || !C.work0, PMK_ERR_ARG);
+    const double *ixm = C.ix ? C.ix : C.sx;
+    const bool chain = C.kind == PMK_COARSE_EIG && ny > 1 && (C.n_cx > 0 || C.n_cy > 0);
     if (ny == 1) {
       int rc = gemm(rows, nx, nx, rhs, nx, 0, C.sx, nx, 0, C.work0, nx, 0, 1, live, s);
       if (rc) return rc;
-      {
-        prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
-        dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work0, C.delta, C.beta,
-                                                             C.dropped, C.n_steps, m, 1.0, live);
-      }
-      PMK_LAUNCH_CHECK();
-      rc = gemm(rows, nx, nx, C.work0, nx, 0, C.sx, nx, 0, out, nx, 0, 1, live, s);
+      rc = run_recurrence(C, C.work0, m, 1.0, C.work1, live, s);
+      if (rc) return rc;
+      rc = gemm(rows, nx, nx, C.work0, nx, 0, ixm, nx, 0, out, nx, 0, 1, live, s);
       if (rc) return rc;
     } else {
       PMK_RETURN_IF(!C.sy || !C.work1, PMK_ERR_ARG);
-      // X S_x over all (slice, y) rows
+      const double *iym = C.iy ? C.iy : C.sy;
+      // X Fx over all (slice, y) rows
       int rc = gemm(rows * ny, nx, nx, rhs, nx, 0, C.sx, nx, 0, C.work0, nx, 0, 1, live, s);
       if (rc) return rc;
-      // S_y X_k per slice
+      // Fy X_k per slice
       rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work0, nx, m, C.work1, nx, m, rows, live, s);
       if (rc) return rc;
-      {
+      if (chain) {
+        rc = launch_eig_chain(C, C.work1, live, s);
+        if (rc) return rc;
+      } else {
         prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
         dst_recurrence_kernel<<<(m + 255) / 256, 256, 0, s>>>(C.work1, C.delta, C.beta,
                                                              C.dropped, C.n_steps, m, 1.0, live);
       }
       PMK_LAUNCH_CHECK();
-      rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work1, nx, m, C.work0, nx, m, rows, live, s);
+      rc = gemm(ny, nx, ny, iym, ny, 0, C.work1, nx, m, C.work0, nx, m, rows, live, s);
       if (rc) return rc;
-      rc = gemm(rows * ny, nx, nx, C.work0, nx, 0, C.sx, nx, 0, out, nx, 0, 1, live, s);
+      rc = gemm(rows * ny, nx, nx, C.work0, nx, 0, ixm, nx, 0, out, nx, 0, 1, live, s);
       if (rc) return rc;
     }
     // out_0 = rhs_0 exactly (stepper.py:118)

@@ -339,7 +339,7 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
   }
   const double units = elems / (N - 1);
   const int grid = (int)(need < (int64_t)occ * kSMs ? need : (int64_t)occ * kSMs);
-  prof::Scope scope(prof::kGemm, 16.0 * elems, units * (5.0 * N * LOGN + 8.0 * N), s);
+  prof::Scope scope(prof::kDst, 16.0 * elems, units * (5.0 * N * LOGN + 8.0 * N), s);
   if (COLS)
     kern<<<grid, 32 * kDstWarps, smem, s>>>(in, out, nx, (int)rows_or_slices, tw2, post, live);
   else {

@@ -127,6 +127,8 @@ enum Cat {
   kRec,       // coarsest per-mode recurrence
   kCoarseMisc,// coarsest dense chain / row copy
   kXfer,      // stand-alone restrict / interpolate / agglomeration gather
+  kDst,       // coarsest FFT sine transforms (pmk_dst.cu)
+  kChain,     // coarsest mode chain with low-rank coupling (EIG, 2-D)
   kNumCat
 };
 struct Scope {

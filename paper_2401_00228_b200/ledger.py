@@ -38,7 +38,8 @@ _CATEGORY_PHASE = {
     "mgs_pass": "orthogonalization",
     "transfer": "restriction",
     "coarse_gemm": "coarse_solve", "coarse_recurrence": "coarse_solve",
-    "coarse_misc": "coarse_solve",
+    "coarse_misc": "coarse_solve", "coarse_dst": "coarse_solve",
+    "coarse_chain": "coarse_solve",
     "reduce": "krylov_other", "fgmres_small": "krylov_other", "assemble": "krylov_other",
 }
 

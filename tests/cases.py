@@ -39,6 +39,7 @@ class Case:
     n_cgs: int = 0
     restart: int | None = None
     two_level_family: str | None = None   # use build_two_level(family) instead
+    perturb: str | None = None   # "rowscale": A -> diag(w) A (not build_laplacian's)
 
     @property
     def ny(self) -> int:
@@ -87,6 +88,24 @@ class Case:
             return u.ravel()
         raise ValueError(self.u0)
 
+    def spatial_matrix(self, a):
+        """The case's spatial operator from build_laplacian's matrix `a`:
+        unchanged, or row-scaled by w_i = 1 + 0.3 sin(2 pi i / n) (a
+        variable-diffusivity operator: non-symmetric, not separable in 2-D)."""
+        if self.perturb is None:
+            return a
+        if self.perturb == "rowscale":
+            import scipy.sparse as sp
+
+            n = a.shape[0]
+            w = 1.0 + 0.3 * np.sin(2.0 * np.pi * np.arange(n) / n)
+            return (sp.diags(w) @ a).tocsr()
+        raise ValueError(self.perturb)
+
+    def schedule_arg(self):
+        """The build_hierarchy schedule argument: "auto" or a list of moves."""
+        return "auto" if self.schedule == "auto" else list(self.schedule)
+
     def scaled(self, **kw) -> "Case":
         d = dict(self.__dict__)
         d.update(kw)
@@ -133,6 +152,45 @@ SMALL = {
                              courant=0.16, two_level_family="MGRIT", n_cgs=4, max_outer=40),
 }
 
+# Round-2 coverage (golden from the live reference): the default "auto"
+# schedule where the stability screen fires (space moves), grids whose n + 1
+# is not a power of two (dense sine-transform GEMMs; MGRIT's GEMM path), and
+# agglomerated coarsest levels (EIG: separable eigen-transforms, 2-D B^T
+# coupling correction on odd grids; even grids need none).
+SMALL.update({
+    "auto_small": Case("auto_small", 2, 15, 32, 0.5, 4, "auto", courant=3.0, max_outer=40),
+    "np2_1d_small": Case("np2_1d_small", 1, 20, 32, 0.5, 3, ("time", "time"), courant=0.64,
+                         max_outer=40),
+    "np2_2d_small": Case("np2_2d_small", 2, 12, 16, 1.0, 3, ("time", "time"), courant=0.16,
+                         max_outer=40),
+    "np2_mgrit_small": Case("np2_mgrit_small", 2, 12, 16, 0.5, 2, ("MGRIT",), nu=2,
+                            courant=0.16, two_level_family="MGRIT", max_outer=40),
+    "even_space_small": Case("even_space_small", 2, 12, 16, 0.5, 3, ("space", "time"),
+                             courant=0.16, max_outer=40),
+    "rowscale_small": Case("rowscale_small", 2, 15, 32, 0.5, 3, ("time", "time"),
+                           courant=0.16, perturb="rowscale", max_outer=40),
+    "rowscale_1d_small": Case("rowscale_1d_small", 1, 31, 32, 0.5, 2, ("time",),
+                              courant=0.64, perturb="rowscale", max_outer=40),
+    "space_dec_small": Case("space_dec_small", 2, 15, 24, 0.5, 3, ("time", "space"),
+                            courant=0.16, n_cgs=3, max_outer=40),
+})
+
+# Mid-size cases (fingerprints, not full vectors: tests/golden/make_golden.py
+# --mid): realistic agglomerated coarsest levels.
+MID = {
+    # 1-D: coarsest 511 points x 129 slices, tridiagonal non-symmetric (3-wide group)
+    "agg1_mid": Case("agg1_mid", 1, 1023, 256, 0.5, 3, ("time", "space"), courant=0.64,
+                     max_outer=60),
+    # the spatial-coarsening switch at the end of a time hierarchy: 127^2 -> 63^2
+    "ttts_mid": Case("ttts_mid", 2, 127, 256, 0.5, 5, ("time", "time", "time", "space"),
+                     courant=0.16, max_outer=60),
+    # the default schedule at a Courant number where time moves fail the screen
+    "auto_mid": Case("auto_mid", 2, 63, 128, 0.5, 4, "auto", courant=3.0, max_outer=60),
+    # the headline grid with the switch: 255^2 x 512, coarsest 127^2 x 64 slices
+    "ttts_255": Case("ttts_255", 2, 255, 512, 0.5, 5, ("time", "time", "time", "space"),
+                     courant=0.16, max_outer=60),
+}
+
 # BASELINE.json configs (literal) and their regime-adjusted companions.
 BASELINE = {
     "c1": Case("c1", 1, 63, 256, 1.0, 2, ("time",), T=1.0, n_cgs=128),
@@ -156,6 +214,23 @@ BASELINE = {
 }
 
 
+MID_STRIDE = 97
+
+
+def fingerprint(v, rows):
+    """A vector at a fixed stride plus the l2 norm of every time slice (the
+    mid-size fixtures; the vectors themselves are too large to commit)."""
+    v = np.asarray(v).ravel()
+    return {"sub": np.ascontiguousarray(v[::MID_STRIDE]),
+            "norms": np.linalg.norm(v.reshape(rows, -1), axis=1)}
+
+
+def mid_inputs(case, hier_sizes):
+    """Seeded (coarsest rhs, fine vector) of the mid-size records."""
+    rng = np.random.default_rng(4321)
+    return rng.standard_normal(hier_sizes[0]), rng.standard_normal(hier_sizes[1])
+
+
 def oracle_hierarchy(case: Case):
     """Build the CPU oracle hierarchy for a case (test infrastructure)."""
     from oracle import pintmk_oracle as O
@@ -166,12 +241,15 @@ def oracle_hierarchy(case: Case):
     if case.two_level_family == "MGRIT":
         return O.build_mgrit(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
                              case.u0_vector(), cfg, nu=case.nu)
+    a = None
+    if case.perturb is not None:
+        a = case.spatial_matrix(O.laplacian(case.dim, case.nx, case.ny)[0])
     if case.two_level_family is not None:
         fam = {"T": ["time"], "TS": ["time_space"]}[case.two_level_family]
         return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
-                       case.u0_vector(), 2, fam, cfg, nu=case.nu)
+                       case.u0_vector(), 2, fam, cfg, nu=case.nu, a=a)
     return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
-                   case.u0_vector(), case.n_levels, list(case.schedule), cfg, nu=case.nu)
+                   case.u0_vector(), case.n_levels, case.schedule_arg(), cfg, nu=case.nu, a=a)
 
 
 def gpu_hierarchy(case: Case, u0=None):
@@ -179,6 +257,9 @@ def gpu_hierarchy(case: Case, u0=None):
     import paper_2401_00228_b200 as P
 
     op = P.build_laplacian(case.dim, case.nx, case.ny if case.dim == 2 else 1)
+    if case.perturb is not None:
+        op = P.SpatialOperator(op.dim, op.n_x, op.n_y, op.delta_x, op.tau,
+                               case.spatial_matrix(op.matrix))
     ops = P.build_step_operators(op, P.ThetaSchemeConfig(case.theta, case.dt(), case.n_t))
     fine = P.FineSystem(ops, case.u0_vector() if u0 is None else u0)
     cfg = P.SolverConfig(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
@@ -186,4 +267,4 @@ def gpu_hierarchy(case: Case, u0=None):
                          restart=case.restart)
     if case.two_level_family is not None:
         return P.build_two_level(fine, case.two_level_family, case.nu, cfg)
-    return P.build_hierarchy(fine, case.n_levels, list(case.schedule), cfg, nu=case.nu)
+    return P.build_hierarchy(fine, case.n_levels, case.schedule_arg(), cfg, nu=case.nu)

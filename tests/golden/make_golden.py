@@ -2,7 +2,8 @@
 container that has /root/reference; the fixtures travel, the reference does
 not).
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py [names]        # small cases (full vectors)
+    python tests/golden/make_golden.py --mid [names]  # mid cases (fingerprints)
 
 For each small case in tests/cases.py it builds the hierarchy with the
 reference's own public API (solver.build_hierarchy / build_two_level; the
@@ -36,14 +37,17 @@ from tests.cases import SMALL  # noqa: E402
 
 def reference_hierarchy(case):
     op = R_sp.build_laplacian(case.dim, case.nx, case.ny if case.dim == 2 else 1)
+    if case.perturb is not None:
+        op = R_sp.SpatialOperator(op.dim, op.n_x, op.n_y, op.delta_x, op.tau,
+                                  case.spatial_matrix(op.matrix))
     ops = R_st.build_step_operators(op, R_st.ThetaSchemeConfig(case.theta, case.dt(), case.n_t))
     fine = R_st.FineSystem(ops, case.u0_vector())
     cfg = R_sol.SolverConfig(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
                              inner_iters=case.inner_iters, coarsest_n_cgs=case.n_cgs)
     if case.two_level_family is not None:
         return R_sol.build_two_level(fine, case.two_level_family, case.nu, cfg)
-    if "time_space" not in case.schedule:
-        return R_sol.build_hierarchy(fine, case.n_levels, list(case.schedule), cfg, nu=case.nu)
+    if case.schedule == "auto" or "time_space" not in case.schedule:
+        return R_sol.build_hierarchy(fine, case.n_levels, case.schedule_arg(), cfg, nu=case.nu)
     levels = [R_sol._fine_level(fine)]
     for mv in case.schedule:
         if mv == "time":
@@ -118,7 +122,46 @@ def record(case) -> dict:
     return out
 
 
+from tests.cases import MID_STRIDE, fingerprint, mid_inputs  # noqa: E402
+
+
+def record_mid(case) -> dict:
+    """Fingerprints only (the vectors are too large to commit): the
+    coarsest forward_solve and apply_preconditioner of seeded inputs, and the
+    full solve (iterations, history, true residual, x)."""
+    hier = reference_hierarchy(case)
+    lv = hier.levels
+    cs_in, pc_in = mid_inputs(case, (lv[-1].total_dim, lv[0].total_dim))
+    out = {"u0": case.u0_vector(), "stride": np.array(MID_STRIDE)}
+    cs = lv[-1].system.forward_solve(cs_in)
+    f = fingerprint(cs, lv[-1].n_steps + 1)
+    out["cs_sub"], out["cs_norms"] = f["sub"], f["norms"]
+    pc = R_sol.apply_preconditioner(hier, 0, pc_in)
+    f = fingerprint(pc, lv[0].n_steps + 1)
+    out["pc_sub"], out["pc_norms"] = f["sub"], f["norms"]
+    x, rep = R_sol.multilevel_solve(hier)
+    out["iters"] = np.array(rep.outer_iterations)
+    out["hist"] = np.array(rep.residual_history)
+    f = fingerprint(x, lv[0].n_steps + 1)
+    out["x_sub"], out["x_norms"] = f["sub"], f["norms"]
+    out["true_res"] = np.array(hier.fine.relative_residual(x))
+    out["moves"] = np.array(hier.moves)
+    return out
+
+
 def main(names=None):
+    if names and names[0] == "--mid":
+        from tests.cases import MID
+
+        for name, case in MID.items():
+            if len(names) > 1 and name not in names[1:]:
+                continue
+            data = record_mid(case)
+            path = os.path.join(HERE, f"{name}.npz")
+            np.savez_compressed(path, **data)
+            print(f"{name}: iters={int(data['iters'])} true_res={float(data['true_res']):.3e} "
+                  f"-> {os.path.getsize(path) / 1024:.0f} KiB", flush=True)
+        return
     for name, case in SMALL.items():
         if names and name not in names:
             continue

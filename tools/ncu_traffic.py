@@ -16,7 +16,8 @@ CATS = [(r"march_tma(?:_1d)?_kernel<(?:\(int\))?0", "march_mv"),
         (r"march_(?:tma(?:_1d)?|lean)_kernel<(?:\(int\))?2", "march_imv"),
         (r"mgs_pass|icwy_dots|icwy_update", "mgs_pass"),
         (r"dot_partials|diffsq_partials", "reduce"), (r"assemble", "assemble"),
-        (r"dst_rows|dst_cols|dgemm", "coarse_gemm"),
+        (r"dst_rows|dst_cols", "coarse_dst"),
+        (r"dgemm", "coarse_gemm"),
         (r"dst_recurrence|rec_chunk", "coarse_recurrence"), (r"copy_row", "coarse_misc")]
 
 
