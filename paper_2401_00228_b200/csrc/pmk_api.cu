@@ -713,12 +713,12 @@ int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaSt
   // Deferred first orthogonalisation: step 0's update pass (w_0 -= h_00 v_0,
   // 24 B per unknown) is fused into step 1's K-MVR, which reads w_0 and v_0
   // anyway-adjacent (+8 B): 2-D constant-stencil time pairs, lazy basis.
+  const bool iso = iso_stencil(R.L.diag_t) && iso_stencil(R.L.sub_t);
   const bool fuse = fuse01() && lazy && R.budget >= 2 && !R.P.mgrit && !R.P.group_of &&
-                    R.L.dim == 2 && !R.L.diag_t.var && !R.L.sub_t.var && !R.L.dropped &&
-                    child_scalable(H, idx);
+                    R.L.dim == 2 && iso && !R.L.dropped && child_scalable(H, idx);
   // budget 1: no update pass at all (h_10 from ||w||^2, see finish_col_block)
   const bool pyth1 = fuse01() && lazy && R.budget == 1 && !R.P.mgrit && !R.P.group_of &&
-                     R.L.dim == 2 && !R.L.diag_t.var && !R.L.sub_t.var && !R.L.dropped;
+                     R.L.dim == 2 && iso && !R.L.dropped;
   for (int j = 0; j < R.budget; ++j) {
     // lazy basis: v_0 is the rhs, step j's w goes to slot j+1 (it is basis
     // vector j+1), the last step's w only feeds ||w|| (w_buf)

@@ -197,6 +197,14 @@ struct MarchParams {
   const int *live;
 };
 
+// Constant stencil with equal off-diagonal slots (S = W = E = N; 1-D: the
+// absent S/N slots are ignored when zero).
+inline bool iso_stencil(const pmk_stencil &st) {
+  if (st.var) return false;
+  const double o = st.c[1];
+  return st.c[3] == o && (st.c[0] == o || st.c[0] == 0.0) && (st.c[4] == o || st.c[4] == 0.0);
+}
+
 // Launch one fused march.  Returns the number of partials written (IMV) via
 // *n_partials when non-null.
 int launch_march(int mode, const MarchParams &p, cudaStream_t s, int *n_partials);

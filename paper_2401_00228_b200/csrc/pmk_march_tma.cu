@@ -360,9 +360,18 @@ __global__ void __launch_bounds__(kTmaThreads)
             b = qcst;
           }
           double Pu, Qu;
-          if (FMA) {  // in-solver passes: fused, same ascending column order
+          if (FMA) {
+            // in-solver passes on isotropic constant stencils (S = W = E = N,
+            // checked by the launcher; every pristine level): the neighbour
+            // sum is formed once and shared by D^T u and B^T u
+#ifndef PMK_NO_ISO
+            const double s4 = (up + lf) + (rt + dn);
+            Pu = fma(a.w, s4, a.c * cur);
+            Qu = fma(b.w, s4, b.c * cur);
+#else  // (A/B: two full 5-point stencils, round-1 form)
             Pu = fma(a.n, dn, fma(a.e, rt, fma(a.c, cur, fma(a.w, lf, __dmul_rn(a.s, up)))));
             Qu = fma(b.n, dn, fma(b.e, rt, fma(b.c, cur, fma(b.w, lf, __dmul_rn(b.s, up)))));
+#endif
           } else {  // separately rounded: bitwise the reference's sparse product
             Pu = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(a.s, up), __dmul_rn(a.w, lf)),
                                                __dmul_rn(a.c, cur)),
@@ -855,9 +864,17 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
 
 // Returns 1 when the TMA path handled the launch, 0 when the caller should
 // use the register path (no driver entry point, unaligned base, N >= 2^31).
-int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_partials,
+int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_partials,
                      double bytes, int cat, int *handled) {
   *handled = 0;
+  MarchParams p = p_in;
+  // the in-solver (FMA) instantiations assume isotropic constant stencils
+  // (S = W = E = N: every pristine level); others take the exact kernels
+  const bool iso = iso_stencil(p.P) && iso_stencil(p.Q);
+  if (p.fma && !(p.P.var || p.Q.var) && !iso) {
+    if (p.v_sub) return PMK_ERR_ARG;  // (fgmres_fixed only fuses isotropic levels)
+    p.fma = 0;
+  }
   const int64_t N = (int64_t)(p.n_steps + 1) * p.m;
   if (N + 2 * kBox >= (int64_t)1 << 31) return 0;
   CUtensorMap mv, mvt;
@@ -873,6 +890,7 @@ int launch_march_tma(int mode, const MarchParams &p, cudaStream_t s, int *n_part
   }
   if (p.v_scale && p.exact_scale) return 0;       // correctly rounded division
   const bool var = p.P.var || p.Q.var;
+
   const bool d2 = p.ny > 1;
   const bool wide1d = !d2 && p.nx > kBox - 1;  // 1-D rows of several segments
   const bool scaled = p.v_scale != nullptr;
