@@ -227,7 +227,10 @@ def run_ours(args):
 
         pdist.init("nccl")
     # replicas: every rank solves its own seeded instance (no data-path collective)
-    case = BASELINE[args.case].scaled(seed=pdist.instance_seed(BASELINE[args.case].seed, rank))
+    from tests.cases import MID
+
+    base = {**MID, **BASELINE}[args.case]
+    case = base.scaled(seed=pdist.instance_seed(base.seed, rank))
     u0 = torch.from_numpy(case.u0_vector()).cuda()
     hier = gpu_hierarchy(case, u0=u0)
 
@@ -361,7 +364,7 @@ def run_ours(args):
             "data": "synthetic (seeded u0 = sin(pi x) sin(pi y) + 0.1 N(0,1); no dataset)",
             "config": {"workload": case.name, "grid": f"{case.nx}x{case.ny}", "n_t": case.n_t,
                        "theta": case.theta, "levels": case.n_levels, "nu": case.nu,
-                       "schedule": list(case.schedule), "courant": case.courant,
+                       "schedule": case.schedule_arg(), "courant": case.courant,
                        "coarsest_n_cgs": case.n_cgs, "restart": case.restart, "tol": case.tol,
                        "unknowns": case.N, "per_rank_instances": 1,
                        "l2": "inputs larger than L2 (2.13 GB vectors), no flush needed"},
@@ -425,19 +428,20 @@ def matvec_roofline(hier, case, steps: int):
 # at a fixed budget, and c5_c_dec: BASELINE config 5's literal solver
 # structure (n_cgs = 256, one independent solve per coarse slice, FGMRES(30))
 # at the paper's Courant number, to 1e-8.
-EXTRA = [("c1_c", None), ("c2_c", None), ("c3_c", None), ("c4_c", 40), ("c5", 30),
-         ("c5_c_dec", None)]
+EXTRA = [("c1_c", None), ("c2_c", None), ("c3_c", None), ("c4", 10), ("c4_c", 40),
+         ("c5", 30), ("c5_c_dec", None), ("ttts_255", None)]
 
 
 def extra_workloads():
     import torch
 
     from paper_2401_00228_b200 import multilevel_solve
-    from tests.cases import BASELINE, gpu_hierarchy
+    from tests.cases import BASELINE, MID, gpu_hierarchy
 
     out = {}
     for name, budget in EXTRA:
-        case = BASELINE[name] if budget is None else BASELINE[name].scaled(max_outer=budget)
+        base = {**MID, **BASELINE}[name]
+        case = base if budget is None else base.scaled(max_outer=budget)
         try:
             u0 = torch.from_numpy(case.u0_vector()).cuda()
             h = gpu_hierarchy(case, u0=u0)
@@ -456,7 +460,7 @@ def extra_workloads():
             ms = e0.elapsed_time(e1) / reps
             out[name] = {
                 "unknowns": case.N, "grid": f"{case.nx}x{case.ny}", "n_t": case.n_t,
-                "theta": case.theta, "levels": case.n_levels, "schedule": list(case.schedule),
+                "theta": case.theta, "levels": case.n_levels, "schedule": case.schedule_arg(),
                 "nu": case.nu, "courant": case.courant, "T": case.T,
                 "coarsest_n_cgs": case.n_cgs, "restart": case.restart,
                 "budget": budget, "ms_per_solve": round(ms, 3),
