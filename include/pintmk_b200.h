@@ -333,6 +333,14 @@ int64_t pmk_launch_count(void);
 int pmk_div_check(const double *x, double d, int64_t n, double *out,
                   pmk_stream_t stream);
 
+/* The coarsest transforms' batched GEMM, exposed for tests and
+ * measurement: C[b] = A[b] B[b] for b < batch, row-major fp64 (element
+ * strides stride_* between batches), on the fp64 tensor cores (DMMA). */
+int pmk_dgemm(int32_t M, int32_t N, int32_t K, const double *A, int32_t lda,
+              int64_t stride_a, const double *B, int32_t ldb, int64_t stride_b,
+              double *C, int32_t ldc, int64_t stride_c, int32_t batch,
+              pmk_stream_t stream);
+
 /* Library identification (for the loaded-.so checks). */
 const char *pmk_version(void);
 

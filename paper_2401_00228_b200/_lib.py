@@ -105,6 +105,8 @@ SIGNATURES = {
     "pmk_fgmres_snapshot": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "pmk_fgmres_snapshot_read": (c_int32, [c_void_p, c_int32, c_int32, c_void_p]),
     "pmk_div_check": (c_int32, [c_void_p, c_double, c_int64, c_void_p, c_void_p]),
+    "pmk_dgemm": (c_int32, [c_int32, c_int32, c_int32, c_void_p, c_int32, c_int64, c_void_p,
+                            c_int32, c_int64, c_void_p, c_int32, c_int64, c_int32, c_void_p]),
 }
 
 _lib = None

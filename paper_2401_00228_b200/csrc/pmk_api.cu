@@ -769,6 +769,16 @@ int pmk_div_check(const double *x, double d, int64_t n, double *out, pmk_stream_
   return launch_div_check(x, d, n, out, cs(stream));
 }
 
+int pmk_dgemm(int32_t M, int32_t N, int32_t K, const double *A, int32_t lda, int64_t stride_a,
+              const double *B, int32_t ldb, int64_t stride_b, double *C, int32_t ldc,
+              int64_t stride_c, int32_t batch, pmk_stream_t stream) {
+  PMK_RETURN_IF(!A || !B || !C || M < 0 || N < 0 || K < 0 || batch < 0, PMK_ERR_ARG);
+  PMK_RETURN_IF(lda < K || ldb < N || ldc < N, PMK_ERR_SHAPE);
+  if (M == 0 || N == 0 || batch == 0) return 0;
+  return launch_gemm(M, N, K, A, lda, stride_a, B, ldb, stride_b, C, ldc, stride_c, batch,
+                     cs(stream));
+}
+
 int pmk_profile_begin(int32_t with_events) {
   std::lock_guard<std::mutex> g(g_prof_mu);
   g_recs.clear();

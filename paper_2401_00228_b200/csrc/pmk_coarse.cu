@@ -21,6 +21,8 @@
 // differs from the reference's LU / Thomas solve by rounding only.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "pmk_internal.cuh"
 
 namespace pmk {
@@ -111,8 +113,124 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Same product on the fp64 tensor cores: mma.sync m8n8k4 (SASS DMMA.8x8x4).
+// CTA tile 64 x 64, 4 warps of 32 x 32 (4 x 4 MMA tiles, 32 accumulators per
+// thread), K staged 16 at a time through shared memory (register double
+// buffering of the next tile's loads).  Fragment layouts (PTX ISA, m8n8k4
+// .f64): A a0 = A[g][t], B b0 = B[t][g], C {c0, c1} = C[g][2t], C[g][2t+1]
+// with g = lane / 4, t = lane % 4.  Shared strides are chosen so that every
+// fragment load is the 2-wavefront minimum: A m-major with row stride 20,
+// B k-major with row stride 72.
+constexpr int TM = 64, TN = 64, TK = 16, SA = TK + 4, SB = TN + 8;
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(128)
+    dmma_gemm_kernel(int M, int N, int K, const double *__restrict__ A, int lda, int64_t sA,
+                     const double *__restrict__ B, int ldb, int64_t sB, double *__restrict__ C,
+                     int ldc, int64_t sC, int batch, const int *live) {
+  if (!is_live(live)) return;
+  __shared__ double As[2][TM][SA];
+  __shared__ double Bs[2][TK][SB];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  const int mtiles = (M + TM - 1) / TM;
+  for (int64_t bt = (int64_t)blockIdx.z * gridDim.y + blockIdx.y; bt < (int64_t)batch * mtiles;
+       bt += (int64_t)gridDim.z * gridDim.y) {
+    const int bz = (int)(bt / mtiles);
+    const double *__restrict__ Ab = A + bz * sA;
+    const double *__restrict__ Bb = B + bz * sB;
+    double *__restrict__ Cb = C + bz * sC;
+    const int m0 = (int)(bt % mtiles) * TM, n0 = blockIdx.x * TN;
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double ra[8], rb[8];
+    auto gload = [&](int k0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = t + 128 * q;
+        const int r = e >> 4, c = e & 15;  // A: 64 rows x 16 k
+        const int gm = m0 + r, gk = k0 + c;
+        ra[q] = (gm < M && gk < K) ? Ab[(int64_t)gm * lda + gk] : 0.0;
+        const int rk = e >> 6, cn = e & 63;  // B: 16 k x 64 columns
+        const int bk = k0 + rk, bn = n0 + cn;
+        rb[q] = (bk < K && bn < N) ? Bb[(int64_t)bk * ldb + bn] : 0.0;
+      }
+    };
+    auto sstore = [&](int buf) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = t + 128 * q;
+        As[buf][e >> 4][e & 15] = ra[q];
+        Bs[buf][e >> 6][e & 63] = rb[q];
+      }
+    };
+    const int nk = (K + TK - 1) / TK;
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    for (int kt = 0; kt < nk; ++kt) {
+      const int buf = kt & 1;
+      if (kt + 1 < nk) gload((kt + 1) * TK);
+#pragma unroll
+      for (int ks = 0; ks < TK; ks += 4) {
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = As[buf][wm + 8 * i + g][ks + tg];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][ks + tg][wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+      }
+      if (kt + 1 < nk) sstore(buf ^ 1);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + wm + 8 * i + g;
+      if (gm >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = n0 + wn + 8 * j + 2 * tg + h;
+          if (gn < N) Cb[(int64_t)gm * ldc + gn] = acc[i][j][h];
+        }
+    }
+  }
+}
+
+// PMK_GEMM=simt selects the CUDA-core kernel (A/B); default: DMMA
+bool gemm_simt() {
+  static const bool on = [] {
+    const char *e = getenv("PMK_GEMM");
+    return e && e[0] == 's';
+  }();
+  return on;
+}
+
 int gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B, int ldb,
          int64_t sB, double *C, int ldc, int64_t sC, int batch, const int *live, cudaStream_t s) {
+  if (!gemm_simt()) {
+    const int mt = (M + TM - 1) / TM;
+    dim3 grid((N + TN - 1) / TN, mt < 4096 ? mt : 4096, batch < 1024 ? batch : 1024);
+    prof::Scope scope(prof::kGemm, 8.0 * batch * ((double)M * N * 2.0) + 8.0 * (double)K * N,
+                      2.0 * M * N * (double)K * batch, s);
+    dmma_gemm_kernel<<<grid, 128, 0, s>>>(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch,
+                                          live);
+    PMK_LAUNCH_CHECK();
+    return 0;
+  }
   const int mtiles = (M + BM - 1) / BM;
   const int gy = mtiles < 4096 ? mtiles : 4096;
   const int gz = batch < 1024 ? batch : 1024;
@@ -583,6 +701,11 @@ int launch_eig_chain(const pmk_coarse &C, double *X, const int *live, cudaStream
 }
 
 }  // namespace
+
+int launch_gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B,
+                int ldb, int64_t sB, double *C, int ldc, int64_t sC, int batch, cudaStream_t s) {
+  return gemm(M, N, K, A, lda, sA, B, ldb, sB, C, ldc, sC, batch, nullptr, s);
+}
 
 // MgritPair.restrict (intergrid.py:152-155): vh[K] = v[nu K].
 int mgrit_restrict(const pmk_pair &P, const double *v, double *vh, const int *live,

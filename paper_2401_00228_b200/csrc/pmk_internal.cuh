@@ -235,6 +235,9 @@ int mgrit_interpolate(const pmk_pair &P, const double *w, double *out, const int
                       cudaStream_t s);
 int launch_dst_cols(const double *in, double *out, int nx, int ny, int slices,
                     const double *tables, const int *live, cudaStream_t s);
+// batched row-major fp64 GEMM C[b] = A[b] B[b] (DMMA; PMK_GEMM=simt: CUDA cores)
+int launch_gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B,
+                int ldb, int64_t sB, double *C, int ldc, int64_t sC, int batch, cudaStream_t s);
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
                  cudaStream_t s, const double *out_scale = nullptr);
 

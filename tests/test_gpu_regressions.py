@@ -96,3 +96,25 @@ def test_restarted_solve_launches_only_library_kernels():
     names = {e.name for e in prof.events() if e.device_type.name == "CUDA"}
     torch_kernels = [n for n in names if "at::" in n or "elementwise" in n.lower()]
     assert not torch_kernels, torch_kernels
+
+
+@pytest.mark.parametrize("m,n,k,batch", [(1, 1, 1, 1), (65, 127, 127, 1), (127, 127, 127, 9),
+                                         (8255, 127, 127, 1), (31, 20, 31, 70),
+                                         (255, 255, 255, 3)])
+def test_dmma_gemm_matches_torch_fp64(m, n, k, batch):
+    """The coarsest transforms' GEMM (fp64 tensor cores) against torch's fp64
+    matmul (a floating-point kernel: torch fp64 reference, 1e-13 relative)."""
+    import torch
+
+    from paper_2401_00228_b200 import _lib
+
+    g = torch.Generator(device="cuda").manual_seed(7)
+    a = torch.randn(batch, m, k, dtype=torch.float64, device="cuda", generator=g)
+    b = torch.randn(batch, k, n, dtype=torch.float64, device="cuda", generator=g)
+    c = torch.full((batch, m, n), float("nan"), dtype=torch.float64, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.pmk_dgemm(m, n, k, _lib.ptr(a), k, m * k, _lib.ptr(b), n, k * n, _lib.ptr(c),
+                             n, m * n, batch, _lib.stream_ptr()), "dgemm")
+    ref = torch.bmm(a, b)
+    err = (torch.linalg.vector_norm(c - ref) / torch.linalg.vector_norm(ref)).item()
+    assert err <= 1e-13, err
