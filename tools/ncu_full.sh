@@ -7,7 +7,7 @@ T=${1:-r1}
 run() {  # name regex skip
   ncu --set full --clock-control none --import-source on -k "regex:$2" --launch-skip $3 \
     --launch-count 1 -o gpurun_out/${T}_$1 -f python bench.py --case c5_c --steps 1 --warmup 0 \
-    --e2e-steps 0 --no-cpu-baseline --no-profile > gpurun_out/${T}_$1.log 2>&1
+    --e2e-steps 0 --no-cpu-baseline --no-profile --no-extra > gpurun_out/${T}_$1.log 2>&1
   echo "$1 rc $?"
 }
 run mvr_fine march_tma 0
