@@ -433,7 +433,10 @@ class CoarseSolver:
             d.dinv = dinv_t.data_ptr()
             d.coupling = self._coupling.desc()
             self._keep.append(dinv_t)
-            self.work0 = torch.empty(self.m, dtype=torch.float64, device="cuda")
+            self._set_chains(d, torch)
+            # one work row per chain (cooperative chain kernel)
+            self.work0 = torch.empty(max(d.n_seg, 1) * self.m, dtype=torch.float64,
+                                     device="cuda")
             self.work1 = None
             self.kind = "dense"
         d.work0 = self.work0.data_ptr()
@@ -471,19 +474,23 @@ class CoarseSolver:
             d.n_cy = fac.corr_y[0].shape[0]
             put("cy_h", fac.corr_y[0])
             put("cy_u", fac.corr_y[1])
-        cuts = sorted(int(c) for c in self._dropped if c > 1)
-        starts = np.array([1] + cuts, dtype=np.int32) if self.n_steps >= 1 else \
-            np.array([1], dtype=np.int32)
-        st = torch.from_numpy(starts).cuda()
-        keep.append(st)
-        d.seg_start = st.data_ptr()
-        d.n_seg = int(starts.size) if self.n_steps >= 1 else 0
+        self._set_chains(d, torch)
         self._keep += keep
         self.factors = fac
         self.work0 = torch.empty(self.N, dtype=torch.float64, device="cuda")
         self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
         self.kind = "eig"
         self.kind_detail = "eig-chain" if (d.n_cx or d.n_cy) else "eig"
+
+    def _set_chains(self, d, torch) -> None:
+        """First row of every independent chain (reference segment_rows,
+        stepper.py:107-112): 1 and each dropped row > 1."""
+        cuts = sorted(int(c) for c in self._dropped if c > 1)
+        starts = np.array([1] + cuts, dtype=np.int32)
+        st = torch.from_numpy(starts).cuda()
+        self._keep.append(st)
+        d.seg_start = st.data_ptr()
+        d.n_seg = int(starts.size) if self.n_steps >= 1 else 0
 
     def solve_into(self, rhs, out) -> None:
         lib = _lib.load()

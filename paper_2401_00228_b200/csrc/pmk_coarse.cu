@@ -415,6 +415,87 @@ __global__ void gemv_kernel(const double *__restrict__ Dinv, const double *__res
   if (lane == 0) out[row] = acc;
 }
 
+// DENSE chain (5-point operators that are not separable): every chain of
+// the level advances one row per step in ONE cooperative launch -- phase A
+// forms b = rhs_k + [k not cut] C out_{k-1} for all chains, phase B applies
+// D^{-1} (a warp per (chain, row) dot product), grid-wide barriers between
+// phases.  Independent chains (perturb_decouple) run side by side.
+__global__ void __launch_bounds__(256)
+    dense_chain_kernel(const double *__restrict__ rhs, double *__restrict__ out,
+                       const double *__restrict__ Dinv, pmk_stencil Cst, int nx, int ny,
+                       const uint8_t *dropped, const int32_t *seg_start, int n_seg, int n_steps,
+                       double *__restrict__ b, const int *live) {
+  namespace cg = cooperative_groups;
+  if (!is_live(live)) return;
+  cg::grid_group grid = cg::this_grid();
+  const int m = nx * ny;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = gtid; i < m; i += gsz) out[i] = rhs[i];  // out_0 = rhs_0
+  int maxlen = 0;
+  for (int sg = 0; sg < n_seg; ++sg) {
+    const int end = (sg + 1 < n_seg) ? seg_start[sg + 1] : n_steps + 1;
+    maxlen = max(maxlen, end - seg_start[sg]);
+  }
+  grid.sync();
+  const int64_t work = (int64_t)n_seg * m;
+  for (int t = 0; t < maxlen; ++t) {
+    for (int64_t e = gtid; e < work; e += gsz) {
+      const int sg = (int)(e / m), i = (int)(e - (int64_t)sg * m);
+      const int a = seg_start[sg];
+      const int end = (sg + 1 < n_seg) ? seg_start[sg + 1] : n_steps + 1;
+      const int k = a + t;
+      if (k >= end) continue;
+      const double *rk = rhs + (int64_t)k * m;
+      if (t == 0 && dropped && dropped[k]) {
+        b[e] = rk[i];
+        continue;
+      }
+      const double *prev = out + (int64_t)(k - 1) * m;
+      const int y = i / nx, x = i - y * nx;
+      double cs_, cw, cc, ce, cn;
+      if (Cst.var) {
+        cs_ = Cst.coef[i];
+        cw = Cst.coef[m + i];
+        cc = Cst.coef[2 * m + i];
+        ce = Cst.coef[3 * m + i];
+        cn = Cst.coef[4 * m + i];
+      } else {
+        cs_ = Cst.c[0];
+        cw = Cst.c[1];
+        cc = Cst.c[2];
+        ce = Cst.c[3];
+        cn = Cst.c[4];
+      }
+      double acc = 0.0;
+      if (y > 0) acc = __dadd_rn(acc, __dmul_rn(cs_, prev[i - nx]));
+      if (x > 0) acc = __dadd_rn(acc, __dmul_rn(cw, prev[i - 1]));
+      acc = __dadd_rn(acc, __dmul_rn(cc, prev[i]));
+      if (x < nx - 1) acc = __dadd_rn(acc, __dmul_rn(ce, prev[i + 1]));
+      if (y < ny - 1) acc = __dadd_rn(acc, __dmul_rn(cn, prev[i + nx]));
+      b[e] = __dadd_rn(rk[i], acc);
+    }
+    grid.sync();
+    for (int64_t w = gwarp; w < work; w += nwarps) {
+      const int sg = (int)(w / m), row = (int)(w - (int64_t)sg * m);
+      const int a = seg_start[sg];
+      const int end = (sg + 1 < n_seg) ? seg_start[sg + 1] : n_steps + 1;
+      const int k = a + t;
+      if (k >= end) continue;
+      const double *dr = Dinv + (int64_t)row * m;
+      const double *bs = b + (int64_t)sg * m;
+      double acc = 0.0;
+      for (int j = lane; j < m; j += 32) acc = fma(dr[j], bs[j], acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) out[(int64_t)k * m + row] = acc;
+    }
+    grid.sync();
+  }
+}
+
 // dst[K * dstride + doff + i] = src[K * sstride + soff + i], i < m, K < rows
 __global__ void strided_rows_copy_kernel(const double *src, int64_t sstride, int64_t soff,
                                          double *dst, int64_t dstride, int64_t doff, int m,
@@ -847,7 +928,7 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
       rc = gemm(ny, nx, ny, C.sy, ny, 0, C.work0, nx, m, C.work1, nx, m, rows, live, s);
       if (rc) return rc;
       if (chain) {
-        rc = launch_eig_chain(C, C.work1, live, s);
+        if (C.n_steps > 0) rc = launch_eig_chain(C, C.work1, live, s);
         if (rc) return rc;
       } else {
         prof::Scope rs(prof::kRec, 16.0 * N, 0.0, s);
@@ -868,7 +949,32 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     PMK_LAUNCH_CHECK();
     return 0;
   }
-  if (C.kind == PMK_COARSE_DENSE) {
+  if (C.kind == PMK_COARSE_DENSE && C.seg_start && C.n_seg >= 1) {
+    PMK_RETURN_IF(!C.dinv || !C.work0, PMK_ERR_ARG);
+    static int blocks = 0;
+    if (!blocks) {
+      int b = 0;
+      PMK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, dense_chain_kernel, 256, 0));
+      blocks = (b > 0 ? b : 1) * kSMs;
+    }
+    const double steps = (double)(C.n_steps + 1);
+    prof::Scope cs(prof::kChain, 8.0 * m * (double)m * C.n_seg + 32.0 * m * steps,
+                   2.0 * m * (double)m * steps, s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    PMK_CUDA_TRY(cudaLaunchKernelEx(&cfg, dense_chain_kernel, rhs, out, C.dinv, C.coupling, nx,
+                                    ny, C.dropped, C.seg_start, C.n_seg, C.n_steps, C.work0,
+                                    live));
+    return 0;
+  }
+  if (C.kind == PMK_COARSE_DENSE) {  // (no chain table: one launch pair per slice)
     PMK_RETURN_IF(!C.dinv || !C.work0, PMK_ERR_ARG);
     {
       prof::Scope cs(prof::kCoarseMisc, 16.0 * m, 0.0, s);

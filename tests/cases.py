@@ -169,6 +169,8 @@ SMALL.update({
                              courant=0.16, max_outer=40),
     "rowscale_small": Case("rowscale_small", 2, 15, 32, 0.5, 3, ("time", "time"),
                            courant=0.16, perturb="rowscale", max_outer=40),
+    "rowscale_dec_small": Case("rowscale_dec_small", 2, 15, 32, 1.0, 2, ("time",),
+                               courant=0.16, perturb="rowscale", n_cgs=5, max_outer=40),
     "rowscale_1d_small": Case("rowscale_1d_small", 1, 31, 32, 0.5, 2, ("time",),
                               courant=0.64, perturb="rowscale", max_outer=40),
     "space_dec_small": Case("space_dec_small", 2, 15, 24, 0.5, 3, ("time", "space"),
