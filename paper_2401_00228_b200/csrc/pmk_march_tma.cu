@@ -31,6 +31,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "pmk_internal.cuh"
@@ -71,6 +72,30 @@ __device__ __forceinline__ void tma_row(double *dst, const CUtensorMap *map, int
       : "memory");
 }
 
+// Same row box as a plain bulk copy (64-bit global address, no tensor map):
+// the vectors whose coordinates exceed int32 (N >= 2^31 doubles).  Without a
+// tensor map there is no out-of-range zero fill, so the box is clipped to
+// [0, n) (16-byte granules); the clipped elements sit at row positions the
+// kernels never read (x = -1 of the first row, past the end of the last).
+// Returns the bytes requested.
+__device__ __forceinline__ uint32_t bulk_bytes(int64_t c, int64_t n) {
+  int64_t lo = c < 0 ? 0 : c, hi = c + kBox;
+  const int64_t nr = (n + 1) & ~(int64_t)1;  // (16-byte granules)
+  if (hi > nr) hi = nr;
+  return hi > lo ? (uint32_t)((hi - lo) * 8) : 0u;
+}
+__device__ __forceinline__ void bulk_row(double *dst, const double *base, int64_t c, int64_t n,
+                                         uint64_t *bar) {
+  const int64_t lo = c < 0 ? 0 : c;
+  const uint32_t bytes = bulk_bytes(c, n);
+  if (!bytes) return;
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst + (lo - c))),
+      "l"(reinterpret_cast<uint64_t>(base + lo)), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 struct Coef5 {
   double s, w, c, e, n;
 };
@@ -101,6 +126,8 @@ __device__ __forceinline__ double stencil5(const Coef5 &a, bool hs, double vs, b
 }
 
 struct TmaGeom {
+  int bulk;         // 1: plain bulk copies from p.v / p.vt / p.v_sub (no tensor maps)
+  int64_t n_v, n_vt;  // their lengths (bulk clipping)
   int single;  // 1: one column tile per row, box starts at x = 0
   int tile_w;  // output columns per tile (1-D: per segment)
   int nseg;    // 1-D: column segments per row
@@ -197,11 +224,35 @@ __global__ void __launch_bounds__(kTmaThreads)
       if (y0 - 1 + rhi > ny - 1) rhi = ny - 1 - (y0 - 1);
     }
     const uint32_t tx_bytes = (uint32_t)(NB * (rhi - rlo + 1) * kBox * sizeof(double));
+    const double *vt_src = kSub ? p.v_sub : p.vt;
 
     auto issue = [&](int k, int stage) {
       double *sv = smem + (size_t)stage * NB * ROWS * kBox;
-      mbar_expect_tx(&bars[stage], tx_bytes);
       const int K = (k == 0) ? 0 : (k - 1) / p.nu + 1;
+      if (g.bulk) {
+        uint32_t bytes = 0;
+        for (int r = rlo; r <= rhi; ++r) {
+          const int y = (DIM == 2) ? y0 - 1 + r : 0;
+          const int64_t c = (int64_t)k * m + (int64_t)y * nx + boxx;
+          bytes += bulk_bytes(c & ~(int64_t)1, g.n_v);
+          if (NB == 2) {
+            const int64_t cv = kSub ? c : (int64_t)K * p.m_coarse + (int64_t)y * nx + boxx;
+            bytes += bulk_bytes(cv & ~(int64_t)1, g.n_vt);
+          }
+        }
+        mbar_expect_tx(&bars[stage], bytes);
+        for (int r = rlo; r <= rhi; ++r) {
+          const int y = (DIM == 2) ? y0 - 1 + r : 0;
+          const int64_t c = (int64_t)k * m + (int64_t)y * nx + boxx;
+          bulk_row(sv + r * kBox, p.v, c & ~(int64_t)1, g.n_v, &bars[stage]);
+          if (NB == 2) {
+            const int64_t cv = kSub ? c : (int64_t)K * p.m_coarse + (int64_t)y * nx + boxx;
+            bulk_row(sv + (ROWS + r) * kBox, vt_src, cv & ~(int64_t)1, g.n_vt, &bars[stage]);
+          }
+        }
+        return;
+      }
+      mbar_expect_tx(&bars[stage], tx_bytes);
       for (int r = rlo; r <= rhi; ++r) {
         const int y = (DIM == 2) ? y0 - 1 + r : 0;
         const int c = (int)((int64_t)k * m + (int64_t)y * nx + boxx);
@@ -599,8 +650,25 @@ __global__ void __launch_bounds__(kTmaThreads)
 
     auto issue = [&](int k, int stage) {
       double *sv = smem + (size_t)stage * NB * R * kBox;
-      mbar_expect_tx(&bars[stage], tx_bytes);
       const int K = (k == 0) ? 0 : (k - 1) / p.nu + 1;
+      if (g.bulk) {
+        uint32_t bytes = 0;
+        for (int r = 0; r < cnt; ++r) {
+          bytes += bulk_bytes(((int64_t)k * m + boxx + r * W) & ~(int64_t)1, g.n_v);
+          if (NB == 2)
+            bytes += bulk_bytes(((int64_t)K * p.m_coarse + boxx + r * W) & ~(int64_t)1, g.n_vt);
+        }
+        mbar_expect_tx(&bars[stage], bytes);
+        for (int r = 0; r < cnt; ++r) {
+          bulk_row(sv + r * kBox, p.v, ((int64_t)k * m + boxx + r * W) & ~(int64_t)1, g.n_v,
+                   &bars[stage]);
+          if (NB == 2)
+            bulk_row(sv + (R + r) * kBox, p.vt,
+                     ((int64_t)K * p.m_coarse + boxx + r * W) & ~(int64_t)1, g.n_vt, &bars[stage]);
+        }
+        return;
+      }
+      mbar_expect_tx(&bars[stage], tx_bytes);
       for (int r = 0; r < cnt; ++r) {
         const int c = (int)((int64_t)k * m + boxx + r * W);
         tma_row(sv + r * kBox, &tm_v, c & ~1, &bars[stage]);
@@ -802,7 +870,7 @@ bool encode_1d(CUtensorMap *map, const double *base, int64_t n) {
 
 template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA = false>
 int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
-            int *n_partials, double bytes, int cat) {
+            int *n_partials, double bytes, int cat, bool bulk) {
   constexpr int NB = ((MODE == kModeIMV && !GATHER) || (MODE == kModeMVR && GATHER)) ? 2 : 1;
   constexpr int ROWS = (DIM == 2) ? R + 2 : R;
   const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
@@ -816,6 +884,9 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
     occ = b > 0 ? b : 1;
   }
   TmaGeom g;
+  g.bulk = bulk ? 1 : 0;
+  g.n_v = (int64_t)(p.n_steps + 1) * p.m;
+  g.n_vt = (MODE == kModeIMV && !GATHER) ? (int64_t)(p.n_steps / p.nu + 1) * p.m_coarse : g.n_v;
   g.single = p.nx <= kBox - 1 ? 1 : 0;  // row + parity shift fits one box
   if (g.single) {
     g.tile_w = p.nx;
@@ -848,9 +919,9 @@ int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt,
   static const bool dbg = getenv("PMK_DEBUG") != nullptr;
   if (dbg)
     fprintf(stderr, "[pmk] tma mode %d dim %d R %d S %d var %d gather %d: nx %d ny %d steps %d "
-            "grid %d smem %zu occ %d single %d tile_w %d gx %d gy %d upc %d chunks %d\n",
+            "grid %d smem %zu occ %d single %d tile_w %d gx %d gy %d upc %d chunks %d bulk %d\n",
             MODE, DIM, R, S, (int)VAR, (int)GATHER, p.nx, p.ny, p.n_steps, grid, smem, occ,
-            g.single, g.tile_w, g.gx, g.gy, g.upc, g.n_chunks);
+            g.single, g.tile_w, g.gx, g.gy, g.upc, g.n_chunks, g.bulk);
   prof::Scope scope(cat, bytes, 0.0, s);
   kern<<<grid, kTmaThreads, smem, s>>>(p, mv, mvt, g);
   PMK_LAUNCH_CHECK();
@@ -876,17 +947,32 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
     p.fma = 0;
   }
   const int64_t N = (int64_t)(p.n_steps + 1) * p.m;
-  if (N + 2 * kBox >= (int64_t)1 << 31) return 0;
-  CUtensorMap mv, mvt;
-  if (!encode_1d(&mv, p.v, N)) return 0;
   const bool gather = (mode == kModeIMV) && p.group_of != nullptr;
-  if (mode == kModeIMV && !gather) {
-    const int64_t Nc = (int64_t)(p.n_steps / p.nu + 1) * p.m_coarse;
-    if (!encode_1d(&mvt, p.vt, Nc)) return 0;
-  } else if (mode == kModeMVR && p.v_sub) {
-    if (!encode_1d(&mvt, p.v_sub, N)) return 0;
+  // 1-D tensor-map coordinates are int32: longer vectors (and PMK_TMA_BULK=1,
+  // for tests) take plain bulk copies with 64-bit addresses instead
+  static const bool force_bulk = [] {
+    const char *e = getenv("PMK_TMA_BULK");
+    return e && e[0] == '1';
+  }();
+  const bool bulk = force_bulk || N + 2 * kBox >= (int64_t)1 << 31;
+  auto al16 = [](const void *q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  CUtensorMap mv, mvt;
+  std::memset(&mv, 0, sizeof(mv));
+  std::memset(&mvt, 0, sizeof(mvt));
+  if (bulk) {
+    if (!al16(p.v) || (mode == kModeIMV && !gather && !al16(p.vt)) ||
+        (mode == kModeMVR && p.v_sub && !al16(p.v_sub)))
+      return 0;
   } else {
-    mvt = mv;
+    if (!encode_1d(&mv, p.v, N)) return 0;
+    if (mode == kModeIMV && !gather) {
+      const int64_t Nc = (int64_t)(p.n_steps / p.nu + 1) * p.m_coarse;
+      if (!encode_1d(&mvt, p.vt, Nc)) return 0;
+    } else if (mode == kModeMVR && p.v_sub) {
+      if (!encode_1d(&mvt, p.v_sub, N)) return 0;
+    } else {
+      mvt = mv;
+    }
   }
   if (p.v_scale && p.exact_scale) return 0;       // correctly rounded division
   const bool var = p.P.var || p.Q.var;
@@ -899,14 +985,14 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
   do {                                                                                         \
     if (var) {                                                                                 \
       rc = scaled ? run_tma<MODE, DIM, R, S, true, GATHER, true>(p, mv, mvt, s, n_partials,     \
-                                                                 bytes, cat)                   \
+                                                                 bytes, cat, bulk)                   \
                   : run_tma<MODE, DIM, R, S, true, GATHER, false>(p, mv, mvt, s, n_partials,    \
-                                                                  bytes, cat);                 \
+                                                                  bytes, cat, bulk);                 \
     } else {                                                                                   \
       rc = scaled ? run_tma<MODE, DIM, R, S, false, GATHER, true>(p, mv, mvt, s, n_partials,    \
-                                                                  bytes, cat)                  \
+                                                                  bytes, cat, bulk)                  \
                   : run_tma<MODE, DIM, R, S, false, GATHER, false>(p, mv, mvt, s, n_partials,   \
-                                                                   bytes, cat);                \
+                                                                   bytes, cat, bulk);                \
     }                                                                                          \
   } while (0)
   // tile rows x ring stages per mode (tuning knob PMK_TMA_CFG=<mvr>,<imv>;
@@ -937,10 +1023,10 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
         }();
         if (tall)
           rc = run_tma<kModeMVR, 2, 8, 2, false, true, false, true>(p, mv, mvt, s, n_partials,
-                                                                     bytes, cat);
+                                                                     bytes, cat, bulk);
         else
           rc = run_tma<kModeMVR, 2, 4, 2, false, true, false, true>(p, mv, mvt, s, n_partials,
-                                                                     bytes, cat);
+                                                                     bytes, cat, bulk);
         break;
       }
       if (d2) {
@@ -950,16 +1036,16 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
           // -3% vs 4x3 by ncu, tools/march_ab_env.sh); PMK_TMA_CFG=4/6,x: 8x2, 4x4
           if (cfg_mvr == 4)
             rc = run_tma<kModeMVR, 2, 8, 2, false, false, true, true>(p, mv, mvt, s, n_partials,
-                                                                       bytes, cat);
+                                                                       bytes, cat, bulk);
           else if (cfg_mvr == 6)
             rc = run_tma<kModeMVR, 2, 4, 4, false, false, true, true>(p, mv, mvt, s, n_partials,
-                                                                       bytes, cat);
+                                                                       bytes, cat, bulk);
           else if (cfg_mvr == 7)
             rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
-                                                                       bytes, cat);
+                                                                       bytes, cat, bulk);
           else
             rc = run_tma<kModeMVR, 2, 8, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
-                                                                       bytes, cat);
+                                                                       bytes, cat, bulk);
           break;
         }
         switch (cfg_mvr) {
@@ -981,10 +1067,10 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
         } else if (p.fma && !var && cfg_imv == 0 && p.out && !p.x_out && p.partials && p.v0 &&
                    !p.dropped) {
           rc = scaled ? run_tma<kModeIMV, 2, 4, 2, false, false, true, true>(p, mv, mvt, s,
-                                                                              n_partials, bytes, cat)
+                                                                              n_partials, bytes, cat, bulk)
                       : run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s,
                                                                                n_partials, bytes,
-                                                                               cat);
+                                                                               cat, bulk);
         } else {
           switch (cfg_imv) {
             case 1: PMK_RUN(kModeIMV, 2, 4, 3, false); break;
