@@ -89,3 +89,25 @@ def test_bulk_copy_path_bitwise_on_golden_cases():
                           env=dict(os.environ, PMK_TMA_BULK="1"), capture_output=True, text=True,
                           timeout=1200, cwd=ROOT)
     assert proc.returncode == 0, proc.stdout[-3000:]
+
+
+def test_dst_gemm_coarsest_beyond_grid_dimension_limits():
+    """The sine-GEMM coarsest path (n + 1 not a power of two) on 100^2 x
+    42000 slices: (slices x 100) / 64 M-tiles exceed the 65535 gridDim.y limit
+    that round 1's GEMM launch put them in.  Size-independent property: the
+    forward substitution inverts the block system, A (A^{-1} r) = r."""
+    import torch
+
+    import paper_2401_00228_b200 as P
+
+    n, steps = 100, 41999
+    op = P.build_laplacian(2, n, n)
+    ops = P.build_step_operators(op, P.ThetaSchemeConfig(0.5, 2e-5, steps))
+    fine = P.FineSystem(ops, torch.zeros(n * n, dtype=torch.float64, device="cuda"))
+    assert fine.diag_factorization.kind_detail == "dst-gemm"
+    g = torch.Generator(device="cuda").manual_seed(3)
+    r = torch.randn((steps + 1) * n * n, dtype=torch.float64, device="cuda", generator=g)
+    u = fine.forward_solve(r)
+    back = fine.matvec(u)
+    err = (torch.linalg.vector_norm(back - r) / torch.linalg.vector_norm(r)).item()
+    assert err <= 1e-12, err
