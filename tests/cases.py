@@ -40,6 +40,7 @@ class Case:
     restart: int | None = None
     two_level_family: str | None = None   # use build_two_level(family) instead
     perturb: str | None = None   # "rowscale": A -> diag(w) A (not build_laplacian's)
+    forcing: str | None = None   # "seeded": g(t, x) = N(0, 1) draws (rng seed + 1)
 
     @property
     def ny(self) -> int:
@@ -87,6 +88,14 @@ class Case:
                     u += a * np.outer(np.sin(q * np.pi * y), np.sin(p * np.pi * x))
             return u.ravel()
         raise ValueError(self.u0)
+
+    def forcing_array(self):
+        """The source term g (n_t, m) of FineSystem (stepper.py:171-185), or None."""
+        if self.forcing is None:
+            return None
+        if self.forcing == "seeded":
+            return np.random.default_rng(self.seed + 1).standard_normal((self.n_t, self.m))
+        raise ValueError(self.forcing)
 
     def spatial_matrix(self, a):
         """The case's spatial operator from build_laplacian's matrix `a`:
@@ -169,6 +178,11 @@ SMALL.update({
                              courant=0.16, max_outer=40),
     "rowscale_small": Case("rowscale_small", 2, 15, 32, 0.5, 3, ("time", "time"),
                            courant=0.16, perturb="rowscale", max_outer=40),
+    # forcing g != 0 and a shift mu != 1 (SolverConfig.mu, solver.py:47)
+    "forced_small": Case("forced_small", 2, 15, 32, 0.5, 3, ("time", "time"), courant=0.16,
+                         forcing="seeded", mu=2.5, max_outer=40),
+    "forced_1d_small": Case("forced_1d_small", 1, 31, 64, 1.0, 3, ("time", "time"),
+                            courant=0.64, forcing="seeded", mu=0.5, n_cgs=3, max_outer=40),
     "rowscale_dec_small": Case("rowscale_dec_small", 2, 15, 32, 1.0, 2, ("time",),
                                courant=0.16, perturb="rowscale", n_cgs=5, max_outer=40),
     "rowscale_1d_small": Case("rowscale_1d_small", 1, 31, 32, 0.5, 2, ("time",),
@@ -255,9 +269,11 @@ def oracle_hierarchy(case: Case):
     if case.two_level_family is not None:
         fam = {"T": ["time"], "TS": ["time_space"]}[case.two_level_family]
         return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
-                       case.u0_vector(), 2, fam, cfg, nu=case.nu, a=a)
+                       case.u0_vector(), 2, fam, cfg, nu=case.nu, a=a,
+                       forcing=case.forcing_array())
     return O.build(case.dim, case.nx, case.ny, case.theta, case.dt(), case.n_t,
-                   case.u0_vector(), case.n_levels, case.schedule_arg(), cfg, nu=case.nu, a=a)
+                   case.u0_vector(), case.n_levels, case.schedule_arg(), cfg, nu=case.nu, a=a,
+                   forcing=case.forcing_array())
 
 
 def gpu_hierarchy(case: Case, u0=None):
@@ -269,7 +285,8 @@ def gpu_hierarchy(case: Case, u0=None):
         op = P.SpatialOperator(op.dim, op.n_x, op.n_y, op.delta_x, op.tau,
                                case.spatial_matrix(op.matrix))
     ops = P.build_step_operators(op, P.ThetaSchemeConfig(case.theta, case.dt(), case.n_t))
-    fine = P.FineSystem(ops, case.u0_vector() if u0 is None else u0)
+    fine = P.FineSystem(ops, case.u0_vector() if u0 is None else u0,
+                        forcing=case.forcing_array())
     cfg = P.SolverConfig(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
                          inner_iters=case.inner_iters, coarsest_n_cgs=case.n_cgs,
                          restart=case.restart)

@@ -41,7 +41,7 @@ def reference_hierarchy(case):
         op = R_sp.SpatialOperator(op.dim, op.n_x, op.n_y, op.delta_x, op.tau,
                                   case.spatial_matrix(op.matrix))
     ops = R_st.build_step_operators(op, R_st.ThetaSchemeConfig(case.theta, case.dt(), case.n_t))
-    fine = R_st.FineSystem(ops, case.u0_vector())
+    fine = R_st.FineSystem(ops, case.u0_vector(), forcing=case.forcing_array())
     cfg = R_sol.SolverConfig(mu=case.mu, tol=case.tol, max_outer=case.max_outer,
                              inner_iters=case.inner_iters, coarsest_n_cgs=case.n_cgs)
     if case.two_level_family is not None:
