@@ -43,7 +43,8 @@ enum {
 };
 
 /* Coarsest-level direct solver kinds (pmk_coarse.kind). */
-enum { PMK_COARSE_DST = 1, PMK_COARSE_DENSE = 2, PMK_COARSE_EIG = 3 };
+enum { PMK_COARSE_DST = 1, PMK_COARSE_DENSE = 2, PMK_COARSE_EIG = 3, PMK_COARSE_PCR = 4,
+       PMK_COARSE_LINE = 5 };
 
 /*
  * Spatial operator in "right-product" form: (v @ M)_i = sum_j M[j,i] v_j,
@@ -127,6 +128,18 @@ typedef struct pmk_pair {
  *      start at seg_start[0..n_seg) (rows; the first is 1).
  * DENSE: explicit D^{-1} (m x m, row-major) for 5-point operators that are
  *      not separable (m <= 8192).
+ * PCR: 1-D levels (D tridiagonal, any coefficients; the reference's Thomas
+ *      chain, _chain.pyx:15-82): parallel cyclic reduction with the matrix
+ *      part factored once -- pcr_alpha/pcr_gamma [pcr_levels][m] multiply the
+ *      right-hand side entries at distance 2^l below / above, pcr_inv [m]
+ *      are the reciprocal final pivots.  One CTA per chain, one launch.
+ * LINE: 2-D 5-point operators of any size that are not separable (the
+ *      reference's per-slice SuperLU solve, stepper.py:140-145,
+ *      linalg.py:35-68): block Thomas over grid lines.  line_g [ny][nx][nx]
+ *      holds the inverted Schur blocks G_j = (T_j - L_j G_{j-1} U_{j-1})^{-1},
+ *      line_l / line_u [m] the couplings D[i, i-nx] / D[i, i+nx].  One CTA
+ *      per chain, one launch; work0 holds n_seg * m doubles.
+ * PCR, LINE and DENSE take `coupling` (C in row form) and the chain table.
  */
 typedef struct pmk_coarse {
   int32_t kind;
@@ -154,6 +167,9 @@ typedef struct pmk_coarse {
   double coupling_b;  /* b in B = I + b K */
   const int32_t *seg_start; /* device [n_seg] first row of each chain */
   int32_t n_seg;
+  int32_t pcr_levels;       /* PCR: ceil(log2 m) reduction strides */
+  const double *pcr_alpha, *pcr_gamma, *pcr_inv;
+  const double *line_g, *line_l, *line_u; /* LINE */
 } pmk_coarse;
 
 /* ---------------------------------------------------------------- per-op */

@@ -348,6 +348,89 @@ class SeparableFactors:
         return 1.0 - lam, 1.0 + self.b * lam
 
 
+def pcr_tables(lower: np.ndarray, diag: np.ndarray, upper: np.ndarray):
+    """Matrix part of parallel cyclic reduction for the tridiagonal system
+    lower[i] x[i-1] + diag[i] x[i] + upper[i] x[i+1] = r[i] (the reference
+    factors the same matrix once with factor_tridiag, _chain.pyx:15-34).
+    Level l (stride s = 2^l) replaces row i by itself plus alpha[l, i] times
+    row i - s plus gamma[l, i] times row i + s, which removes its couplings
+    at distance s and leaves couplings at distance 2 s; after ceil(log2 m)
+    levels every row is diagonal.  Returns (alpha, gamma) of shape
+    (levels, m) and inv = 1 / final pivots: a right-hand side is solved by
+    r <- r + alpha[l] * r[. - s] + gamma[l] * r[. + s] per level, x = r * inv.
+    No pivoting: D = I - a dt A is strictly diagonally dominant for the
+    levels this package builds; a zero pivot raises LinAlgError as the
+    reference's factorisation does (_chain.pyx:29-31)."""
+    m = diag.size
+    levels = int(np.ceil(np.log2(m))) if m > 1 else 0
+    a = np.array(lower, dtype=np.float64)
+    b = np.array(diag, dtype=np.float64)
+    c = np.array(upper, dtype=np.float64)
+    a[0] = 0.0
+    c[-1] = 0.0
+    alpha = np.zeros((levels, m))
+    gamma = np.zeros((levels, m))
+    for lv in range(levels):
+        s = 1 << lv
+        if np.any(b == 0.0):
+            raise np.linalg.LinAlgError("factorization failed: zero pivot in cyclic reduction")
+        al = np.zeros(m)
+        ga = np.zeros(m)
+        al[s:] = -a[s:] / b[:-s]
+        ga[:-s] = -c[:-s] / b[s:]
+        nb = b.copy()
+        nb[s:] += al[s:] * c[:-s]
+        nb[:-s] += ga[:-s] * a[s:]
+        na = np.zeros(m)
+        nc = np.zeros(m)
+        na[s:] = al[s:] * a[:-s]
+        nc[:-s] = ga[:-s] * c[s:]
+        alpha[lv], gamma[lv] = al, ga
+        a, b, c = na, nb, nc
+    if np.any(b == 0.0) or not np.all(np.isfinite(b)):
+        raise np.linalg.LinAlgError("factorization failed: zero pivot in cyclic reduction")
+    return alpha, gamma, 1.0 / b
+
+
+def line_tables(coef: np.ndarray, nx: int, ny: int):
+    """Block-Thomas tables of a 5-point operator D given in row form
+    (coef[s, i], slots S W C E N): D is block tridiagonal over grid lines,
+    with tridiagonal T_j on the diagonal and diagonal couplings
+    L_j = diag(coef[0]) / U_j = diag(coef[4]) to the lines below / above.
+    G_j = (T_j - L_j G_{j-1} U_{j-1})^{-1}, dense nx x nx (the role of the
+    reference's sparse LU, linalg.py:42-55).  Returns G of shape
+    (ny, nx, nx)."""
+    g = np.empty((ny, nx, nx))
+    for j in range(ny):
+        sl = slice(j * nx, (j + 1) * nx)
+        t = np.diag(coef[2, sl])
+        if nx > 1:
+            t += np.diag(coef[1, sl][1:], -1) + np.diag(coef[3, sl][:-1], 1)
+        if j > 0:
+            up_prev = coef[4, (j - 1) * nx:j * nx]
+            t -= coef[0, sl][:, None] * g[j - 1] * up_prev[None, :]
+        try:
+            g[j] = np.linalg.inv(t)
+        except np.linalg.LinAlgError as exc:
+            raise np.linalg.LinAlgError(f"factorization failed: {exc}") from exc
+    return g
+
+
+# 1-D levels with at least this many independent chains take PCR (a CTA per
+# chain) instead of the eigen-transform GEMMs + per-mode recurrence.
+PCR_MIN_CHAINS = 32
+PCR_MAX_M = 9000      # three shared-memory rows of m doubles per CTA
+LINE_MAX_NX = 3072    # two shared-memory lines per CTA
+
+
+def forced_coarse_kind() -> str:
+    """PMK_COARSE_KIND = pcr | line | eig | dense: take that coarsest kind
+    wherever it applies (tests and A/B runs); empty = the default choice."""
+    import os
+
+    return os.environ.get("PMK_COARSE_KIND", "").strip().lower()
+
+
 class CoarseSolver:
     """Device tables of the block forward substitution of one level
     (reference stepper.py:114-146)."""
@@ -367,7 +450,15 @@ class CoarseSolver:
         d = _lib.CoarseDesc()
         d.dim, d.nx, d.ny, d.n_steps = dim, self.nx, self.ny, n_steps
         d.dropped = None if self._mask is None else self._mask.data_ptr()
-        if spectral is not None:
+        forced = forced_coarse_kind()
+        n_chains = 1 + sum(1 for c in self._dropped if c > 1)
+        one_d = self.ny == 1
+        fac = None
+        if forced == "pcr" and one_d and self.nx <= PCR_MAX_M:
+            self._setup_pcr(d, diag, sub, torch)
+        elif forced == "line" and not one_d and self.nx <= LINE_MAX_NX:
+            self._setup_line(d, diag, sub, torch)
+        elif spectral is not None and forced not in ("eig", "dense"):
             d.kind = _lib.PMK_COARSE_DST
             ex = dst_eigenvalues_1d(self.nx)
             tabx = fft_dst_tables(self.nx)
@@ -410,9 +501,18 @@ class CoarseSolver:
             # 2-D: second transform buffer; 1-D: chunked-recurrence scratch
             self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
             self.kind = "dst"
-        elif (fac := SeparableFactors.detect(diag, sub, self.nx, self.ny, dim)) is not None \
-                and (self.nx <= 8192 if self.ny == 1 else (self.nx <= 256 and self.ny <= 512)):
+        elif one_d and n_chains >= PCR_MIN_CHAINS and self.nx <= PCR_MAX_M \
+                and forced not in ("eig", "dense"):
+            # many independent chains (perturb_decouple): a CTA per chain
+            self._setup_pcr(d, diag, sub, torch)
+        elif forced != "dense" \
+                and (fac := SeparableFactors.detect(diag, sub, self.nx, self.ny, dim)) is not None \
+                and (self.nx <= 8192 if one_d else (self.nx <= 256 and self.ny <= 512)):
             self._setup_eig(d, fac, torch)
+        elif one_d and self.nx <= PCR_MAX_M and forced != "dense":
+            self._setup_pcr(d, diag, sub, torch)
+        elif not one_d and self.m > DENSE_MAX_M and self.nx <= LINE_MAX_NX:
+            self._setup_line(d, diag, sub, torch)
         else:
             if self.m > DENSE_MAX_M:
                 raise NotImplementedError(
@@ -481,6 +581,47 @@ class CoarseSolver:
         self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
         self.kind = "eig"
         self.kind_detail = "eig-chain" if (d.n_cx or d.n_cy) else "eig"
+
+    def _coupling_table(self, d, sub) -> None:
+        """C of out_k = D^{-1} (rhs_k + C out_{k-1}) as a row-form stencil:
+        B in 1-D (chain march, _chain.pyx:64-71), B^T in 2-D (stepper.py:144,
+        `out[k-1] @ sub`)."""
+        cmat = sub if self.dim == 1 else sp.csr_matrix(sub).T
+        self._coupling = StencilTable(cmat, self.nx, self.ny)
+        d.coupling = self._coupling.desc()
+
+    def _setup_pcr(self, d, diag, sub, torch) -> None:
+        """PCR tables of a 1-D level (any tridiagonal D)."""
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+        coef = StencilTable(diag, self.nx, 1).coef
+        alpha, gamma, inv = pcr_tables(coef[1], coef[2], coef[3])
+        d.kind = _lib.PMK_COARSE_PCR
+        d.pcr_levels = int(alpha.shape[0])
+        tabs = [dev(alpha if alpha.size else np.zeros(1)),
+                dev(gamma if gamma.size else np.zeros(1)), dev(inv)]
+        d.pcr_alpha, d.pcr_gamma, d.pcr_inv = (t.data_ptr() for t in tabs)
+        self._keep += tabs
+        self._coupling_table(d, sub)
+        self._set_chains(d, torch)
+        self.work0 = torch.empty(1, dtype=torch.float64, device="cuda")
+        self.work1 = None
+        self.kind = self.kind_detail = "pcr"
+
+    def _setup_line(self, d, diag, sub, torch) -> None:
+        """Block-Thomas tables of a 2-D 5-point level of any size."""
+        dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+        coef = StencilTable(diag, self.nx, self.ny).coef
+        g = line_tables(coef, self.nx, self.ny)
+        d.kind = _lib.PMK_COARSE_LINE
+        tabs = [dev(g), dev(coef[0]), dev(coef[4])]
+        d.line_g, d.line_l, d.line_u = (t.data_ptr() for t in tabs)
+        self._keep += tabs
+        self._coupling_table(d, sub)
+        self._set_chains(d, torch)
+        # the y lines of every chain (line_chain_kernel)
+        self.work0 = torch.empty(max(d.n_seg, 1) * self.m, dtype=torch.float64, device="cuda")
+        self.work1 = None
+        self.kind = self.kind_detail = "line"
 
     def _set_chains(self, d, torch) -> None:
         """First row of every independent chain (reference segment_rows,

@@ -25,6 +25,8 @@ PMK_ERR_STATE = 1004
 PMK_COARSE_DST = 1
 PMK_COARSE_DENSE = 2
 PMK_COARSE_EIG = 3
+PMK_COARSE_PCR = 4
+PMK_COARSE_LINE = 5
 
 
 class Stencil(ctypes.Structure):
@@ -56,7 +58,9 @@ class CoarseDesc(ctypes.Structure):
                 ("fft_scale", c_double), ("ix", c_void_p), ("iy", c_void_p),
                 ("n_cx", c_int32), ("n_cy", c_int32), ("cx_h", c_void_p), ("cx_u", c_void_p),
                 ("cy_h", c_void_p), ("cy_u", c_void_p), ("coupling_b", c_double),
-                ("seg_start", c_void_p), ("n_seg", c_int32)]
+                ("seg_start", c_void_p), ("n_seg", c_int32), ("pcr_levels", c_int32),
+                ("pcr_alpha", c_void_p), ("pcr_gamma", c_void_p), ("pcr_inv", c_void_p),
+                ("line_g", c_void_p), ("line_l", c_void_p), ("line_u", c_void_p)]
 
 
 # name -> (restype, argtypes); exactly the functions include/pintmk_b200.h declares

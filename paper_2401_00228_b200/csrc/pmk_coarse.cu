@@ -949,6 +949,16 @@ int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int 
     PMK_LAUNCH_CHECK();
     return 0;
   }
+  if (C.kind == PMK_COARSE_PCR || C.kind == PMK_COARSE_LINE) {
+    {
+      prof::Scope cs(prof::kCoarseMisc, 16.0 * m, 0.0, s);
+      copy_row_kernel<<<(m + 255) / 256, 256, 0, s>>>(rhs, out, m, live);  // stepper.py:118
+    }
+    PMK_LAUNCH_CHECK();
+    if (C.n_steps < 1) return 0;
+    return C.kind == PMK_COARSE_PCR ? launch_pcr_chains(C, rhs, out, live, s)
+                                    : launch_line_chains(C, rhs, out, live, s);
+  }
   if (C.kind == PMK_COARSE_DENSE && C.seg_start && C.n_seg >= 1) {
     PMK_RETURN_IF(!C.dinv || !C.work0, PMK_ERR_ARG);
     static int blocks = 0;

@@ -128,7 +128,7 @@ enum Cat {
   kCoarseMisc,// coarsest dense chain / row copy
   kXfer,      // stand-alone restrict / interpolate / agglomeration gather
   kDst,       // coarsest FFT sine transforms (pmk_dst.cu)
-  kChain,     // coarsest mode chain with low-rank coupling (EIG, 2-D)
+  kChain,     // coarsest chains in one launch: EIG 2-D mode chain, DENSE, PCR, LINE
   kNumCat
 };
 struct Scope {
@@ -238,6 +238,11 @@ int launch_dst_cols(const double *in, double *out, int nx, int ny, int slices,
 // batched row-major fp64 GEMM C[b] = A[b] B[b] (DMMA; PMK_GEMM=simt: CUDA cores)
 int launch_gemm(int M, int N, int K, const double *A, int lda, int64_t sA, const double *B,
                 int ldb, int64_t sB, double *C, int ldc, int64_t sC, int batch, cudaStream_t s);
+// per-slice direct solves without a common eigenbasis (pmk_lines.cu)
+int launch_pcr_chains(const pmk_coarse &C, const double *rhs, double *out, const int *live,
+                      cudaStream_t s);
+int launch_line_chains(const pmk_coarse &C, const double *rhs, double *out, const int *live,
+                       cudaStream_t s);
 int coarse_solve(const pmk_coarse &C, const double *rhs, double *out, const int *live,
                  cudaStream_t s, const double *out_scale = nullptr);
 

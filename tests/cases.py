@@ -205,6 +205,17 @@ MID = {
     # the headline grid with the switch: 255^2 x 512, coarsest 127^2 x 64 slices
     "ttts_255": Case("ttts_255", 2, 255, 512, 0.5, 5, ("time", "time", "time", "space"),
                      courant=0.16, max_outer=60),
+    # a caller's own (row-scaled, non-separable) operator whose coarsest level
+    # has 127^2 = 16129 unknowns per slice: past the dense-inverse limit, the
+    # LINE (block Thomas) coarsest solve; exact chain and 4 decoupled chains
+    "line_mid": Case("line_mid", 2, 127, 32, 0.5, 2, ("time",), courant=0.16,
+                     perturb="rowscale", max_outer=60),
+    "line_dec_mid": Case("line_dec_mid", 2, 127, 32, 1.0, 2, ("time",), courant=0.16,
+                         perturb="rowscale", n_cgs=4, max_outer=30),
+    # 1-D, 32 decoupled chains (16 slices each) of a non-Toeplitz tridiagonal
+    # level: PCR, a CTA per chain
+    "pcr_dec_mid": Case("pcr_dec_mid", 1, 1023, 1024, 0.5, 2, ("time",), courant=0.64,
+                        perturb="rowscale", n_cgs=32, max_outer=60),
 }
 
 # BASELINE.json configs (literal) and their regime-adjusted companions.
