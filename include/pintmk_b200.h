@@ -135,10 +135,13 @@ typedef struct pmk_pair {
  *      are the reciprocal final pivots.  One CTA per chain, one launch.
  * LINE: 2-D 5-point operators of any size that are not separable (the
  *      reference's per-slice SuperLU solve, stepper.py:140-145,
- *      linalg.py:35-68): block Thomas over grid lines.  line_g [ny][nx][nx]
- *      holds the inverted Schur blocks G_j = (T_j - L_j G_{j-1} U_{j-1})^{-1},
- *      line_l / line_u [m] the couplings D[i, i-nx] / D[i, i+nx].  One CTA
- *      per chain, one launch; work0 holds n_seg * m doubles.
+ *      linalg.py:35-68): block Thomas over grid lines.  line_g holds the
+ *      inverted Schur blocks G_j = (T_j - L_j G_{j-1} U_{j-1})^{-1} split by
+ *      rows over the line_cs CTAs of a chain's cluster, R = ceil(nx/line_cs)
+ *      rows each: [ny][line_cs][R][nx] with entry (j, g, r, c) = G_j[g R + r, c]
+ *      (0 past row nx); line_l / line_u [m] are the couplings D[i, i-nx] /
+ *      D[i, i+nx].  One cluster per chain, one launch; work0 holds
+ *      n_seg * 2 m doubles.
  * PCR, LINE and DENSE take `coupling` (C in row form) and the chain table.
  */
 typedef struct pmk_coarse {
@@ -170,6 +173,7 @@ typedef struct pmk_coarse {
   int32_t pcr_levels;       /* PCR: ceil(log2 m) reduction strides */
   const double *pcr_alpha, *pcr_gamma, *pcr_inv;
   const double *line_g, *line_l, *line_u; /* LINE */
+  int32_t line_cs;          /* LINE: CTAs per chain (cluster size, 1..8) */
 } pmk_coarse;
 
 /* ---------------------------------------------------------------- per-op */

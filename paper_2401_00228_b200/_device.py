@@ -416,11 +416,31 @@ def line_tables(coef: np.ndarray, nx: int, ny: int):
     return g
 
 
+def line_cluster_size(n_chains: int) -> int:
+    """CTAs per chain of the LINE kernel: the largest power of two <= 8 that
+    still leaves every chain's cluster resident at once (148 SMs)."""
+    cs = 8
+    while cs > 1 and cs * n_chains > 148:
+        cs //= 2
+    return cs
+
+
+def line_chunks(g: np.ndarray, cs: int) -> np.ndarray:
+    """G (ny, nx, nx) re-laid for a cluster of cs CTAs per chain: CTA q owns
+    rows [q R, q R + R), R = ceil(nx / cs), stored [j][q][r][c] (row-major
+    chunks, zero rows past nx)."""
+    ny, nx, _ = g.shape
+    r = -(-nx // cs)
+    pad = np.zeros((ny, cs * r, nx))
+    pad[:, :nx, :] = g
+    return np.ascontiguousarray(pad.reshape(ny, cs, r, nx))
+
+
 # 1-D levels with at least this many independent chains take PCR (a CTA per
 # chain) instead of the eigen-transform GEMMs + per-mode recurrence.
 PCR_MIN_CHAINS = 32
 PCR_MAX_M = 9000      # three shared-memory rows of m doubles per CTA
-LINE_MAX_NX = 3072    # two shared-memory lines per CTA
+LINE_MAX_NX = 1536    # a line is staged by 512 threads x 3 elements
 
 
 def forced_coarse_kind() -> str:
@@ -613,13 +633,16 @@ class CoarseSolver:
         coef = StencilTable(diag, self.nx, self.ny).coef
         g = line_tables(coef, self.nx, self.ny)
         d.kind = _lib.PMK_COARSE_LINE
-        tabs = [dev(g), dev(coef[0]), dev(coef[4])]
+        n_chains = 1 + sum(1 for c in self._dropped if c > 1)
+        d.line_cs = line_cluster_size(n_chains)
+        tabs = [dev(line_chunks(g, d.line_cs)), dev(coef[0]), dev(coef[4])]
         d.line_g, d.line_l, d.line_u = (t.data_ptr() for t in tabs)
         self._keep += tabs
         self._coupling_table(d, sub)
         self._set_chains(d, torch)
         # the y lines of every chain (line_chain_kernel)
-        self.work0 = torch.empty(max(d.n_seg, 1) * self.m, dtype=torch.float64, device="cuda")
+        self.work0 = torch.empty(max(d.n_seg, 1) * 2 * self.m, dtype=torch.float64,
+                                 device="cuda")
         self.work1 = None
         self.kind = self.kind_detail = "line"
 

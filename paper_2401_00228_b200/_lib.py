@@ -60,7 +60,8 @@ class CoarseDesc(ctypes.Structure):
                 ("cy_h", c_void_p), ("cy_u", c_void_p), ("coupling_b", c_double),
                 ("seg_start", c_void_p), ("n_seg", c_int32), ("pcr_levels", c_int32),
                 ("pcr_alpha", c_void_p), ("pcr_gamma", c_void_p), ("pcr_inv", c_void_p),
-                ("line_g", c_void_p), ("line_l", c_void_p), ("line_u", c_void_p)]
+                ("line_g", c_void_p), ("line_l", c_void_p), ("line_u", c_void_p),
+                ("line_cs", c_int32)]
 
 
 # name -> (restype, argtypes); exactly the functions include/pintmk_b200.h declares

@@ -999,9 +999,7 @@ int pmk_hier_set_level(pmk_hier *H, int32_t idx, const pmk_level *L, const pmk_p
 
 int pmk_hier_set_coarse(pmk_hier *H, const pmk_coarse *C) {
   PMK_RETURN_IF(!H || !C, PMK_ERR_ARG);
-  PMK_RETURN_IF(C->kind != PMK_COARSE_DST && C->kind != PMK_COARSE_DENSE &&
-                    C->kind != PMK_COARSE_EIG,
-                PMK_ERR_UNSUPPORTED);
+  PMK_RETURN_IF(C->kind < PMK_COARSE_DST || C->kind > PMK_COARSE_LINE, PMK_ERR_UNSUPPORTED);
   drop_graphs(H);
   H->coarse = *C;
   H->has_coarse = true;

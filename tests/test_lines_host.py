@@ -132,3 +132,19 @@ def test_pcr_tables_reduce_to_a_diagonal_system():
 def test_zero_pivot_raises_like_the_reference():
     with pytest.raises(np.linalg.LinAlgError, match="factorization failed"):
         pcr_tables(np.zeros(4), np.array([1.0, 0.0, 1.0, 1.0]), np.zeros(4))
+
+
+def test_line_chunks_layout_and_cluster_size():
+    from paper_2401_00228_b200._device import line_chunks, line_cluster_size
+
+    g = np.random.default_rng(5).standard_normal((3, 13, 13))
+    for cs in (1, 2, 4, 8):
+        ch = line_chunks(g, cs)
+        r = -(-13 // cs)
+        assert ch.shape == (3, cs, r, 13)
+        for q in range(cs):
+            for rr in range(r):
+                row = q * r + rr
+                want = g[:, row, :] if row < 13 else np.zeros((3, 13))
+                np.testing.assert_array_equal(ch[:, q, rr, :], want)
+    assert [line_cluster_size(n) for n in (1, 18, 19, 37, 74, 75, 500)] == [8, 8, 4, 4, 2, 1, 1]
