@@ -429,7 +429,8 @@ def matvec_roofline(hier, case, steps: int):
 # structure (n_cgs = 256, one independent solve per coarse slice, FGMRES(30))
 # at the paper's Courant number, to 1e-8.
 EXTRA = [("c1_c", None), ("c2_c", None), ("c3_c", None), ("c4", 10), ("c4_c", 40),
-         ("c5", 30), ("c5_c_dec", None), ("ttts_255", None)]
+         ("c5", 30), ("c5_c_dec", None), ("ttts_255", None), ("c1", 12), ("pcr_dec_mid", None),
+         ("line_mid", None), ("line_dec_mid", None)]
 
 
 def extra_workloads():
@@ -463,6 +464,8 @@ def extra_workloads():
                 "theta": case.theta, "levels": case.n_levels, "schedule": case.schedule_arg(),
                 "nu": case.nu, "courant": case.courant, "T": case.T,
                 "coarsest_n_cgs": case.n_cgs, "restart": case.restart,
+                "coarsest_kind": getattr(h.levels[-1].system.diag_factorization,
+                                         "kind_detail", None),
                 "budget": budget, "ms_per_solve": round(ms, 3),
                 "iterations": rep.outer_iterations,
                 "converged": bool(rep.converged),

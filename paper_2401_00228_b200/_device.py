@@ -436,15 +436,19 @@ def line_chunks(g: np.ndarray, cs: int) -> np.ndarray:
     return np.ascontiguousarray(pad.reshape(ny, cs, r, nx))
 
 
-# 1-D levels with at least this many independent chains take PCR (a CTA per
-# chain) instead of the eigen-transform GEMMs + per-mode recurrence.
-PCR_MIN_CHAINS = 32
+# 1-D levels take PCR (a CTA per chain, (log2 m + 3) block barriers per slice)
+# when the longest chain is at most this many slices: against the FFT sine
+# transforms + per-mode recurrence on pristine levels, against the
+# eigen-transform GEMMs on other tridiagonal levels
+# (profiles/r2_coarse_kinds.md).
+PCR_MAX_CHAIN_VS_DST = 8
+PCR_MAX_CHAIN_VS_EIG = 40
 PCR_MAX_M = 9000      # three shared-memory rows of m doubles per CTA
 LINE_MAX_NX = 1536    # a line is staged by 512 threads x 3 elements
 
 
 def forced_coarse_kind() -> str:
-    """PMK_COARSE_KIND = pcr | line | eig | dense: take that coarsest kind
+    """PMK_COARSE_KIND = pcr | line | eig | dense | dst: take that coarsest kind
     wherever it applies (tests and A/B runs); empty = the default choice."""
     import os
 
@@ -471,13 +475,18 @@ class CoarseSolver:
         d.dim, d.nx, d.ny, d.n_steps = dim, self.nx, self.ny, n_steps
         d.dropped = None if self._mask is None else self._mask.data_ptr()
         forced = forced_coarse_kind()
-        n_chains = 1 + sum(1 for c in self._dropped if c > 1)
+        cuts = sorted(int(c) for c in self._dropped if c > 1)
+        longest = max(b - a for a, b in zip([1] + cuts, cuts + [n_steps + 1])) if n_steps else 0
         one_d = self.ny == 1
+        pcr_fits = one_d and self.nx <= PCR_MAX_M and forced not in ("eig", "dense", "dst")
         fac = None
         if forced == "pcr" and one_d and self.nx <= PCR_MAX_M:
             self._setup_pcr(d, diag, sub, torch)
         elif forced == "line" and not one_d and self.nx <= LINE_MAX_NX:
             self._setup_line(d, diag, sub, torch)
+        elif spectral is not None and pcr_fits and 0 < longest <= PCR_MAX_CHAIN_VS_DST \
+                and forced != "dst":
+            self._setup_pcr(d, diag, sub, torch)
         elif spectral is not None and forced not in ("eig", "dense"):
             d.kind = _lib.PMK_COARSE_DST
             ex = dst_eigenvalues_1d(self.nx)
@@ -521,15 +530,14 @@ class CoarseSolver:
             # 2-D: second transform buffer; 1-D: chunked-recurrence scratch
             self.work1 = torch.empty(self.N, dtype=torch.float64, device="cuda")
             self.kind = "dst"
-        elif one_d and n_chains >= PCR_MIN_CHAINS and self.nx <= PCR_MAX_M \
-                and forced not in ("eig", "dense"):
-            # many independent chains (perturb_decouple): a CTA per chain
+        elif pcr_fits and 0 < longest <= PCR_MAX_CHAIN_VS_EIG:
+            # short independent chains (perturb_decouple): a CTA per chain
             self._setup_pcr(d, diag, sub, torch)
         elif forced != "dense" \
                 and (fac := SeparableFactors.detect(diag, sub, self.nx, self.ny, dim)) is not None \
                 and (self.nx <= 8192 if one_d else (self.nx <= 256 and self.ny <= 512)):
             self._setup_eig(d, fac, torch)
-        elif one_d and self.nx <= PCR_MAX_M and forced != "dense":
+        elif pcr_fits:
             self._setup_pcr(d, diag, sub, torch)
         elif not one_d and self.m > DENSE_MAX_M and self.nx <= LINE_MAX_NX:
             self._setup_line(d, diag, sub, torch)

@@ -2,8 +2,11 @@
 (tests/golden/make_golden.py --mid): realistic agglomerated coarsest levels
 (the EIG coarsest solve -- separable eigen-transforms, per-mode recurrence,
 the cluster chain kernel for the odd-grid B^T coupling), the default "auto"
-schedule where the stability screen inserts space moves, and the spatial
-coarsening switch at the end of a time hierarchy on 127^2 and 255^2 grids.
+schedule where the stability screen inserts space moves, the spatial
+coarsening switch at the end of a time hierarchy on 127^2 and 255^2 grids,
+and a caller's own row-scaled operator whose coarsest level takes the LINE
+(2-D, 16129 unknowns per slice, past the dense-inverse limit) and PCR (1-D,
+32 decoupled chains) kinds by default.
 
 Bars: coarsest forward_solve <= 1e-12 relative (rounding: eigen-transforms vs
 the reference's SuperLU / Thomas), apply_preconditioner <= 1e-10, full solve
@@ -21,6 +24,10 @@ from tests.cases import MID, fingerprint, gpu_hierarchy, mid_inputs
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# cases whose coarsest level takes a kind from csrc/pmk_lines.cu by default
+DEFAULT_KIND = {"line_mid": "line", "line_dec_mid": "line", "pcr_dec_mid": "pcr"}
 
 
 def rel(a, b):
@@ -58,6 +65,8 @@ def test_mid_parity(name):
     coarse = lv[-1].system.diag_factorization
     if any(m in ("space", "time_space") for m in h.moves):
         assert coarse.kind == "eig", coarse.kind
+    if name in DEFAULT_KIND:
+        assert coarse.kind == DEFAULT_KIND[name], coarse.kind
     cs_in, pc_in = mid_inputs(case, (lv[-1].total_dim, lv[0].total_dim))
     cs = lv[-1].system.forward_solve(torch.from_numpy(cs_in).cuda()).cpu().numpy()
     f = fingerprint(cs, lv[-1].n_steps + 1)
