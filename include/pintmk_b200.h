@@ -104,6 +104,17 @@ typedef struct pmk_pair {
   double fft_scale;
   const double *ratio;
   double *work0, *work1, *work2, *coarse_out;
+  /* Weighted space pair (z_ptr != NULL; group_of = NULL): an extension with
+   * no reference counterpart -- BASELINE config 4 names full-weighting
+   * restriction and bilinear interpolation, the reference only agglomerates
+   * (intergrid.py:79-131).  Restriction is the time sum followed by the Y^T
+   * CSR above with general weights; interpolation applies the CSR Z over
+   * fine points (z_ptr [m_fine+1], z_idx coarse indices ascending, z_val
+   * weights) and repeats in time.  In the solver the coarse solution goes to
+   * coarse_out ((n_T+1) m_coarse doubles) and its space interpolation
+   * ((n_T+1) m_fine) is the iteration's child vector. */
+  const int32_t *z_ptr, *z_idx;
+  const double *z_val;
 } pmk_pair;
 
 /*

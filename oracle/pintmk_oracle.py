@@ -14,8 +14,14 @@ Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline leg may
 import this module, and only as the checker.  The product package
 (paper_2401_00228_b200) never imports it and has no CPU fallback.
 
-Extension (new knob, not in the reference): `restarted_solve` = FGMRES(m)
-built from the reference's own fgmres cycles.
+Extensions (not in the reference): `restarted_solve` = FGMRES(m) built from
+the reference's own fgmres cycles; and the
+"space_fw" / "time_space_fw" moves (`make_fw_pair`, `_space_rung_fw`):
+full-weighting restriction, (bi)linear interpolation and a rediscretised
+coarse Laplacian, the transfers BASELINE config 4 names and the reference
+does not have.  PARITY UNPINNED for that extension: there is no reference
+output to pin it to; everything around it (matvec, fgmres, coarsest solve)
+is the pinned code above.
 """
 
 from __future__ import annotations
@@ -232,7 +238,9 @@ class Pair:
 
     @property
     def m(self) -> int:
-        return self.n if self.groups is None else len(self.groups)
+        if self.groups is None:
+            return self.n if self.y is None else self.y.shape[1]
+        return len(self.groups)
 
 
 def make_ts_pair(nu, n_T, groups, n) -> Pair:
@@ -244,6 +252,33 @@ def make_ts_pair(nu, n_T, groups, n) -> Pair:
     return Pair(nu, n_T, n, groups, y, z)
 
 
+def fw_1d(count: int):
+    """EXTENSION (no reference counterpart): 1-D full weighting R (n_c x n,
+    rows 1/4 1/2 1/4 centred on fine point 2 c + 1) and linear interpolation
+    P = 2 R^T between n and n_c = (n - 1) / 2 interior points."""
+    if count < 3 or count % 2 == 0:
+        raise ValueError("full weighting needs an odd number (>= 3) of interior points")
+    nc = (count - 1) // 2
+    r = sp.lil_matrix((nc, count))
+    for c in range(nc):
+        r[c, 2 * c], r[c, 2 * c + 1], r[c, 2 * c + 2] = 0.25, 0.5, 0.25
+    r = r.tocsr()
+    return r, (2.0 * r.T).tocsr()
+
+
+def make_fw_pair(nu, n_T, nx, ny, dim) -> Pair:
+    """EXTENSION: full-weighting / (bi)linear pair; y (n x m) restricts as
+    `summed @ y`, z (n x m) interpolates as `w @ z.T`, like make_ts_pair."""
+    rx, px = fw_1d(nx)
+    if dim == 2:
+        ry, py = fw_1d(ny)
+        r, pz = sp.kron(ry, rx, format="csr"), sp.kron(py, px, format="csr")
+    else:
+        r, pz = rx, px
+    return Pair(nu, n_T, nx * (ny if dim == 2 else 1), None, sp.csr_matrix(r.T),
+                sp.csr_matrix(pz))
+
+
 def restrict(p: Pair, v: np.ndarray) -> np.ndarray:
     """intergrid.py:51-56 / 106-112 / 152-155 (MGRIT injection)."""
     blk = np.ascontiguousarray(v).reshape(p.nu * p.n_T + 1, -1)
@@ -252,7 +287,7 @@ def restrict(p: Pair, v: np.ndarray) -> np.ndarray:
         return out.reshape(-1) if v.ndim == 1 else out
     summed = blk[1:].reshape(p.n_T, p.nu, p.n).sum(axis=1)
     out = np.empty((p.n_T + 1, p.m))
-    if p.groups is None:
+    if p.y is None:
         out[0] = blk[0]
         out[1:] = summed
     else:
@@ -273,7 +308,7 @@ def interpolate(p: Pair, w: np.ndarray) -> np.ndarray:
             cur = np.ascontiguousarray(p.psi_solve((cur @ p.phi).T).T)
             out[j::p.nu] = cur
         return out.reshape(-1) if w.ndim == 1 else out
-    if p.groups is not None:
+    if p.z is not None:
         blk = blk @ p.z.T
     out = np.empty((p.nu * p.n_T + 1, p.n))
     out[0] = blk[0]
@@ -357,6 +392,29 @@ def _space_rung(r: Rung, time_nu: int = 1) -> Rung:
                 "space" if time_nu == 1 else "time_space")
 
 
+def _space_rung_fw(r: Rung, time_nu: int = 1) -> Rung:
+    """EXTENSION (no reference counterpart): full-weighting space move onto
+    the grid with doubled spacing, coarse operator = the Laplacian
+    rediscretised there: (factor / 4) * unit second differences, factor =
+    tau / dx^2 of this rung (read off its pristine matrix)."""
+    gx, gy = r.grid
+    if r.n_steps % time_nu:
+        raise ValueError("time factor must divide n_steps")
+    nT = r.n_steps // time_nu
+    r.pair = make_fw_pair(time_nu, nT, gx, gy, r.dim)
+    mx, my = (gx - 1) // 2, ((gy - 1) // 2 if r.dim == 2 else 1)
+    factor = float(r.a[0, 1]) / 4.0
+    unit, _ = laplacian(r.dim, mx, my, 1.0, float(mx + 1))
+    if r.dim == 2 and my != mx:
+        raise ValueError("oracle fw move: square grids only")
+    ac = (factor * unit).tocsr()
+    w = 1.0 - (1.0 - r.weight) / time_nu
+    dt = time_nu * r.dt
+    d, b = blocks_from(ac, w, dt)
+    return Rung(System(d, b, nT), ac, dt, w, nT, (mx, my), r.dim,
+                "space_fw" if time_nu == 1 else "time_space_fw")
+
+
 def _stable(r: Rung, nu: int) -> bool:
     """solver.py:154-163."""
     expl = (1.0 - r.weight) / nu
@@ -436,6 +494,10 @@ def build(dim, nx, ny, theta, dt, n_t, u0, n_levels, schedule, cfg: Config, nu=2
             rungs.append(_space_rung(cur))
         elif move == "time_space":
             rungs.append(_space_rung(cur, nu))
+        elif move == "space_fw":
+            rungs.append(_space_rung_fw(cur))
+        elif move == "time_space_fw":
+            rungs.append(_space_rung_fw(cur, nu))
         else:
             raise ValueError(f"unknown move {move!r}")
         moves.append(move)

@@ -12,7 +12,7 @@ from .spatial import (SpatialOperator, build_laplacian, courant_number,  # noqa:
                       max_eigenvalue_magnitude)
 from .stepper import (BlockBidiagonalSystem, FineSystem, StepOperators,  # noqa: F401
                       ThetaSchemeConfig, build_step_operators, sequential_solve)
-from .intergrid import (CoarseSystem, MgritPair, TimePair, TimeSpacePair,  # noqa: F401
+from .intergrid import (CoarseSystem, MgritPair, TimePair, TimeSpacePair, WeightedSpacePair,  # noqa: F401
                         agglomerate_partition, perturb_decouple, rediscretized_coarse)
 from .solver import (Level, LevelHierarchy, SolveReport, SolverConfig,  # noqa: F401
                      apply_preconditioner, build_hierarchy, build_two_level, fgmres,

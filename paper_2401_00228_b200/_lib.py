@@ -46,7 +46,8 @@ class PairDesc(ctypes.Structure):
                 ("dim", c_int32), ("nx", c_int32), ("ny", c_int32), ("sx", c_void_p),
                 ("sy", c_void_p), ("fft_x", c_void_p), ("fft_y", c_void_p),
                 ("fft_scale", c_double), ("ratio", c_void_p), ("work0", c_void_p),
-                ("work1", c_void_p), ("work2", c_void_p), ("coarse_out", c_void_p)]
+                ("work1", c_void_p), ("work2", c_void_p), ("coarse_out", c_void_p),
+                ("z_ptr", c_void_p), ("z_idx", c_void_p), ("z_val", c_void_p)]
 
 
 class CoarseDesc(ctypes.Structure):

@@ -196,11 +196,17 @@ int check_pair(const pmk_level &L, const pmk_pair *P) {
     PMK_RETURN_IF(!P->fft_x && !P->sx, PMK_ERR_ARG);
     return 0;
   }
-  const bool space = P->group_of != nullptr;
+  const bool space = P->group_of != nullptr || P->z_ptr != nullptr;
   PMK_RETURN_IF(space && (!P->y_ptr || !P->y_idx || !P->y_val), PMK_ERR_ARG);
   PMK_RETURN_IF(!space && P->m_coarse != P->m_fine, PMK_ERR_SHAPE);
+  PMK_RETURN_IF(P->z_ptr && (P->group_of || !P->z_idx || !P->z_val), PMK_ERR_ARG);
   return 0;
 }
+
+// weighted space pair (full weighting / bilinear): see pmk_pair z_*
+inline bool weighted(const pmk_pair &P) { return P.z_ptr != nullptr; }
+// the iteration's child vector is already at the level's spatial size
+inline bool child_is_fine_space(const pmk_pair &P) { return P.mgrit || weighted(P); }
 
 MarchParams base_params(const pmk_level &L) {
   MarchParams p;
@@ -269,7 +275,7 @@ int do_mvr(const pmk_level &L, const pmk_pair &P, double mu, const double *v,
   p.inject = P.mgrit ? 1 : 0;  // MgritPair.restrict (intergrid.py:152-155)
   p.exact_scale = exact ? 1 : 0;
   p.fma = exact ? 0 : 1;  // in-solver (non-exact) passes may fuse
-  const bool space = P.group_of != nullptr;
+  const bool space = P.group_of != nullptr || weighted(P);
   PMK_RETURN_IF(space && !scratch, PMK_ERR_ARG);
   p.vh = space ? scratch : vh;
   p.live = live;
@@ -297,8 +303,8 @@ int do_imv(const pmk_level &L, const pmk_pair &P, const double *v, const double 
   p.v_scale = v_scale;
   p.nu = P.mgrit ? 1 : P.nu;
   p.vt = vt;
-  p.group_of = P.group_of;
-  p.m_coarse = P.mgrit ? P.m_fine : P.m_coarse;
+  p.group_of = P.group_of;  // (NULL for weighted pairs: vt is space-interpolated)
+  p.m_coarse = child_is_fine_space(P) ? P.m_fine : P.m_coarse;
   p.x_out = x;
   p.out = w;
   p.v0 = v0;
@@ -564,6 +570,14 @@ int fgmres_step(pmk_hier *H, int idx, int j, double *v_out, double *w_next, doub
     if (rc) return rc;
     prof::Tag tag(idx, prof::kHintInterp);
     rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, live, s);
+  } else if (weighted(R.P)) {
+    // coarse solve into the pair's scratch, then Z over space into the
+    // iteration's child vector ((n_T+1) x m_fine; K-IMV repeats it in time)
+    PMK_RETURN_IF(!R.P.coarse_out, PMK_ERR_ARG);
+    rc = child_solve(H, idx, R.P.coarse_out, live, s);
+    if (rc) return rc;
+    prof::Tag tag(idx, prof::kHintInterp);
+    rc = launch_interpolate_z(R.P, R.P.coarse_out, child_out, 1, live, s);
   } else {
     rc = child_solve(H, idx, child_out, live, s, child_scale);
   }
@@ -663,14 +677,15 @@ int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cuda
     if (rc) return rc;
   }
   const int64_t off = (int64_t)row0 * m;
-  const int64_t coff = (int64_t)(row0 / nu) * (R.P.mgrit ? m : R.P.m_coarse);
+  const int mc = child_is_fine_space(R.P) ? m : R.P.m_coarse;
+  const int64_t coff = (int64_t)(row0 / nu) * mc;
   const int64_t n_sub = (int64_t)(row1 - row0) * m;
   const int n = (int)R.vt.size();
   // time pairs with nu = 2 take the pair kernel (<= 8 vectors per pass, every
   // coarse value read once, all loads up front); more vectors are summed in
   // passes of 8 -- two extra x read/write sweeps for 19 vectors still beat
   // the one-pass generic kernel's dependent per-element loop (4.4 TB/s)
-  const bool pair = !R.P.mgrit && !R.P.group_of && R.P.nu == 2 && R.P.m_coarse == m;
+  const bool pair = !R.P.mgrit && !R.P.group_of && R.P.nu == 2 && mc == m;
   const int per_pass = pair ? 8 : kAsmChunk;
   int first = 0;
   do {
@@ -684,9 +699,8 @@ int fgmres_finish_rows(pmk_hier *H, int idx, double *x, int row0, int row1, cuda
     }
     if (R.P.mgrit)  // vt_l are the interpolated fine vectors
       rc = launch_assemble(R.d_state, a, x + off, n_sub, m, 1, m, nullptr, first, s);
-    else
-      rc = launch_assemble(R.d_state, a, x + off, n_sub, m, R.P.nu, R.P.m_coarse,
-                           R.P.group_of, first, s);
+    else  // (weighted pairs: vt_l are interpolated in space already)
+      rc = launch_assemble(R.d_state, a, x + off, n_sub, m, R.P.nu, mc, R.P.group_of, first, s);
     if (rc) return rc;
     first += per_pass;
   } while (first < n);
@@ -714,10 +728,10 @@ int fgmres_fixed(pmk_hier *H, int idx, double *x, const int *parent_live, cudaSt
   // 24 B per unknown) is fused into step 1's K-MVR, which reads w_0 and v_0
   // anyway-adjacent (+8 B): 2-D constant-stencil time pairs, lazy basis.
   const bool iso = iso_stencil(R.L.diag_t) && iso_stencil(R.L.sub_t);
-  const bool fuse = fuse01() && lazy && R.budget >= 2 && !R.P.mgrit && !R.P.group_of &&
+  const bool fuse = fuse01() && lazy && R.budget >= 2 && !R.P.mgrit && !R.P.group_of && !R.P.z_ptr &&
                     R.L.dim == 2 && iso && !R.L.dropped && child_scalable(H, idx);
   // budget 1: no update pass at all (h_10 from ||w||^2, see finish_col_block)
-  const bool pyth1 = fuse01() && lazy && R.budget == 1 && !R.P.mgrit && !R.P.group_of &&
+  const bool pyth1 = fuse01() && lazy && R.budget == 1 && !R.P.mgrit && !R.P.group_of && !R.P.z_ptr &&
                      R.L.dim == 2 && iso && !R.L.dropped;
   for (int j = 0; j < R.budget; ++j) {
     // lazy basis: v_0 is the rhs, step j's w goes to slot j+1 (it is basis
@@ -860,7 +874,7 @@ int pmk_restrict(const pmk_pair *P, const double *v, double *vh, double *scratch
                  pmk_stream_t stream) {
   PMK_RETURN_IF(!P || !v || !vh, PMK_ERR_ARG);
   if (P->mgrit) return mgrit_restrict(*P, v, vh, nullptr, cs(stream));
-  if (P->group_of) {
+  if (P->group_of || P->z_ptr) {
     PMK_RETURN_IF(!scratch, PMK_ERR_ARG);
     pmk_pair tp = *P;
     int rc = launch_restrict_time(tp, v, scratch, cs(stream));
@@ -1019,7 +1033,7 @@ int pmk_hier_set_buffers(pmk_hier *H, int32_t idx, double *rhs, double *const *v
   PMK_RETURN_IF(!R.set, PMK_ERR_STATE);
   PMK_RETURN_IF(n_slots < 0 || (n_slots > 0 && (!v_slots || !child_out || !w_buf)),
                 PMK_ERR_ARG);
-  PMK_RETURN_IF(R.P.group_of && !ts_scratch, PMK_ERR_ARG);
+  PMK_RETURN_IF((R.P.group_of || R.P.z_ptr) && !ts_scratch, PMK_ERR_ARG);
   R.rhs = rhs;
   R.w_buf = w_buf;
   if (idx > 0 && !R.rhs_part)  // the parent's K-MVR leaves ||rhs||^2 partials here
@@ -1128,6 +1142,12 @@ int pmk_apply_preconditioner(pmk_hier *H, int32_t idx, const double *v, double *
     if (rc) return rc;
     prof::Tag itag(idx, prof::kHintInterp);
     rc = mgrit_interpolate(R.P, R.P.coarse_out, child_out, nullptr, s);
+  } else if (weighted(R.P)) {
+    PMK_RETURN_IF(!R.P.coarse_out, PMK_ERR_ARG);
+    rc = child_solve(H, idx, R.P.coarse_out, nullptr, s);
+    if (rc) return rc;
+    prof::Tag itag(idx, prof::kHintInterp);
+    rc = launch_interpolate_z(R.P, R.P.coarse_out, child_out, 1, nullptr, s);
   } else {
     rc = child_solve(H, idx, child_out, nullptr, s);
   }

@@ -251,5 +251,8 @@ int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, cons
                      cudaStream_t s);
 int launch_restrict_time(const pmk_pair &P, const double *v, double *vh, cudaStream_t s);
 int launch_interpolate(const pmk_pair &P, const double *w, double *out, cudaStream_t s);
+// weighted space pair (pmk_pair z_*): Z over space, repeated `nu` times in time
+int launch_interpolate_z(const pmk_pair &P, const double *w, double *out, int nu,
+                         const int *live, cudaStream_t s);
 
 }  // namespace pmk

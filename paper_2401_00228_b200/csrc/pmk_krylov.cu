@@ -818,6 +818,26 @@ __global__ void interpolate_kernel(const double *w, double *out, int nu, int n_T
   }
 }
 
+// Weighted space interpolation (pmk_pair z_*): out[k, i] = sum_q z_val[q] *
+// w[K(k), z_idx[q]], K(k) = coarse slice of fine slice k (nu = 1: the space
+// interpolation of every coarse slice, the solver's child vector).
+__global__ void interpolate_z_kernel(const double *w, double *out, int nu, int rows, int m_fine,
+                                     int m_coarse, const int32_t *ptr, const int32_t *idx,
+                                     const double *val, const int *live) {
+  if (!is_live(live)) return;
+  const int64_t total = (int64_t)rows * m_fine;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = e / m_fine;
+    const int i = (int)(e - k * m_fine);
+    const int64_t K = (k == 0) ? 0 : (k - 1) / nu + 1;
+    const double *row = w + K * m_coarse;
+    double acc = 0.0;
+    for (int q = ptr[i]; q < ptr[i + 1]; ++q) acc = __dadd_rn(acc, __dmul_rn(val[q], row[idx[q]]));
+    out[e] = acc;
+  }
+}
+
 __global__ void div_check_kernel(const double *x, double d, int64_t n, double *out) {
   const double rcp = __drcp_rn(d);
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -1123,7 +1143,19 @@ int launch_ts_gather(const pmk_pair &P, const double *fine, double *coarse, cons
   return 0;
 }
 
+int launch_interpolate_z(const pmk_pair &P, const double *w, double *out, int nu,
+                         const int *live, cudaStream_t s) {
+  const int rows = nu * P.n_T + 1;
+  const int64_t n = (int64_t)rows * P.m_fine;
+  prof::Scope scope(prof::kXfer, 8.0 * n + 8.0 * (double)(P.n_T + 1) * P.m_coarse, 0.0, s);
+  interpolate_z_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, out, nu, rows, P.m_fine, P.m_coarse,
+                                                        P.z_ptr, P.z_idx, P.z_val, live);
+  PMK_LAUNCH_CHECK();
+  return 0;
+}
+
 int launch_interpolate(const pmk_pair &P, const double *w, double *out, cudaStream_t s) {
+  if (P.z_ptr) return launch_interpolate_z(P, w, out, P.nu, nullptr, s);
   const int64_t n = (int64_t)(P.nu * P.n_T + 1) * P.m_fine;
   prof::Scope scope(prof::kXfer, 8.0 * n + 8.0 * (double)(P.n_T + 1) * P.m_coarse, 0.0, s);
   interpolate_kernel<<<grid_for(n, 256), 256, 0, s>>>(w, out, P.nu, P.n_T, P.m_fine, P.m_coarse,

@@ -47,7 +47,7 @@ class _PairBase:
             raise ValueError("vector size does not match the fine level")
         out = torch.empty((self.n_T + 1) * self.m, dtype=torch.float64, device="cuda")
         scratch = None
-        if self.m != self.n or getattr(self, "partition", None) is not None:
+        if self.m != self.n or getattr(self, "partition", None) is not None:  # space pairs
             scratch = torch.empty((self.n_T + 1) * self.n, dtype=torch.float64, device="cuda")
         lib = _lib.load()
         _lib.check(lib.pmk_restrict(ctypes.byref(self._pair_desc()), _lib.ptr(dv), _lib.ptr(out),
@@ -149,6 +149,97 @@ class TimeSpacePair(_PairBase):
             d.group_of, d.y_ptr, d.y_idx, d.y_val = (t.data_ptr() for t in tabs)
             self._desc = d
         return self._desc
+
+    def block_matrices(self, k: int):
+        if k == 0:
+            return self.y_space, self.z_space
+        return (sp.vstack([self.y_space] * self.nu, format="csr"),
+                sp.vstack([self.z_space] * self.nu, format="csr"))
+
+    def materialize(self):
+        ys, zs = zip(*(self.block_matrices(k) for k in range(self.n_T + 1)))
+        return sp.block_diag(ys, format="csr"), sp.block_diag(zs, format="csr")
+
+
+def full_weighting_1d(count: int):
+    """1-D full-weighting restriction R (n_c x n) and linear interpolation
+    P (n x n_c) between n interior points and the n_c = (n - 1) / 2 interior
+    points of the grid with doubled spacing (coarse point c sits on fine point
+    2 c + 1): R rows (1/4, 1/2, 1/4), P = 2 R^T."""
+    if count < 3 or count % 2 == 0:
+        raise ValueError("full weighting needs an odd number (>= 3) of interior points")
+    nc = (count - 1) // 2
+    c = np.arange(nc)
+    rows = np.repeat(c, 3)
+    cols = (2 * c[:, None] + np.arange(3)[None, :]).ravel()
+    vals = np.tile([0.25, 0.5, 0.25], nc)
+    r = sp.csr_matrix((vals, (rows, cols)), shape=(nc, count))
+    return r, (2.0 * r.T).tocsr()
+
+
+class WeightedSpacePair(_PairBase):
+    """Space coarsening by full-weighting restriction and (bi)linear
+    interpolation, optionally with time coarsening by nu -- BASELINE config
+    4's transfer operators.  An EXTENSION: the reference only agglomerates
+    (intergrid.py:79-131), so this pair has no reference counterpart and its
+    parity is pinned to the oracle's restatement of the same formulas only.
+    Same conventions as TimeSpacePair: restrict sums each slab's nu rows and
+    applies y_space^T (rows of weights summing to 1, like agglomerate
+    averaging); interpolate applies z_space (weights 1, 1/2, 1/4) and
+    repeats each coarse row nu times."""
+
+    kind = "TS_FW"
+    partition = None
+
+    def __init__(self, nu: int, n_T: int, grid: tuple[int, int], dim: int):
+        if nu < 1:
+            raise ValueError("nu must be positive")
+        nx, ny = grid[0], (grid[1] if dim == 2 else 1)
+        rx, px = full_weighting_1d(nx)
+        if dim == 2:
+            ry, py = full_weighting_1d(ny)
+            r, pz = sp.kron(ry, rx, format="csr"), sp.kron(py, px, format="csr")
+            self.coarse_grid = (rx.shape[0], ry.shape[0])
+        else:
+            r, pz = rx, px
+            self.coarse_grid = (rx.shape[0], 1)
+        self.nu, self.n_T = nu, n_T
+        self.n, self.m = nx * ny, r.shape[0]
+        self.fine_rows = nu * n_T + 1
+        self.y_space = sp.csr_matrix(r.T)   # (n, m): restrict = v @ y_space
+        self.z_space = sp.csr_matrix(pz)    # (n, m): interpolate = w @ z_space^T
+        self._desc = None
+        self._keep = []
+
+    def _pair_desc(self) -> _lib.PairDesc:
+        if self._desc is None:
+            torch = _lib.require_cuda()
+            yt = sp.csr_matrix(self.y_space.T)
+            yt.sort_indices()
+            z = sp.csr_matrix(self.z_space)
+            z.sort_indices()
+            i32 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).cuda()  # noqa: E731
+            f64 = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+            tabs = [i32(yt.indptr), i32(yt.indices), f64(yt.data),
+                    i32(z.indptr), i32(z.indices), f64(z.data),
+                    torch.empty((self.n_T + 1) * self.m, dtype=torch.float64, device="cuda")]
+            self._keep = tabs
+            d = _lib.PairDesc()
+            d.nu, d.n_T, d.m_fine, d.m_coarse = self.nu, self.n_T, self.n, self.m
+            d.group_of = None
+            d.y_ptr, d.y_idx, d.y_val, d.z_ptr, d.z_idx, d.z_val, d.coarse_out = \
+                (t.data_ptr() for t in tabs)
+            self._desc = d
+        return self._desc
+
+    def child_size(self) -> int:
+        """The solver's per-iteration child vector: the coarse solution
+        interpolated in space ((n_T + 1) x n), repeated in time by K-IMV."""
+        return (self.n_T + 1) * self.n
+
+    def expand_child(self, child):
+        """Z w from a stored child vector (time repeat only)."""
+        return TimePair(self.n, self.nu, self.n_T).interpolate(child)
 
     def block_matrices(self, k: int):
         if k == 0:

@@ -32,7 +32,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from ._device import SpectralInfo
-from .intergrid import (CoarseSystem, MgritPair, TimePair, TimeSpacePair,
+from .intergrid import (CoarseSystem, MgritPair, TimePair, TimeSpacePair, WeightedSpacePair,
                         agglomerate_partition, perturb_decouple, rediscretized_coarse)
 from .spatial import gershgorin_bound
 from .stepper import BlockBidiagonalSystem, FineSystem, _to_device
@@ -228,6 +228,34 @@ def _space_move(level: Level, time_nu: int = 1) -> Level:
                  kind="space" if time_nu == 1 else "time_space")
 
 
+def _space_move_fw(level: Level, time_nu: int = 1) -> Level:
+    """Space coarsening by full weighting / (bi)linear interpolation onto the
+    grid with doubled spacing, optionally with time coarsening: BASELINE
+    config 4's transfers.  EXTENSION without a reference counterpart (the
+    reference's space move agglomerates, solver.py:127-143).  The coarse
+    operator is the Laplacian rediscretised on the coarse grid (the Galerkin
+    product of these transfers is a 9-point operator); it needs a level whose
+    spatial operator is build_laplacian's and odd grid sizes."""
+    from .spatial import laplacian_stencil, stencil_csr
+
+    if level.laplace_factor is None:
+        raise ValueError("full-weighting space moves need build_laplacian's operator")
+    if level.n_steps % time_nu != 0:
+        raise ValueError("time factor must divide n_steps")
+    n_steps = level.n_steps // time_nu
+    pair = WeightedSpacePair(time_nu, n_steps, level.grid, level.dim)
+    level.pair = pair
+    mx, my = pair.coarse_grid
+    factor = level.laplace_factor / 4.0          # tau / (2 dx)^2, exact
+    coarse_a = stencil_csr(mx, my, laplacian_stencil(level.dim, factor))
+    a = 1.0 - (1.0 - level.implicit_weight) / time_nu
+    dt = time_nu * level.dt
+    system = _coarse_system_from(coarse_a, a, dt, n_steps, (mx, my), level.dim, factor)
+    return Level(system=system, spatial_matrix=coarse_a, dt=dt, implicit_weight=a,
+                 n_steps=n_steps, grid=(mx, my), dim=level.dim,
+                 kind="space_fw" if time_nu == 1 else "time_space_fw", laplace_factor=factor)
+
+
 def _fine_level(fine: FineSystem) -> Level:
     ops = fine.ops
     sp_op = ops.spatial
@@ -280,8 +308,11 @@ def build_hierarchy(fine: FineSystem, n_levels: int, schedule: str | list[str] =
                     cfg: SolverConfig | None = None, nu: int = 2) -> LevelHierarchy:
     """Level stack by repeated coarsening (reference solver.py:178-216).
 
-    Moves: "time", "space" (reference) and "time_space" (agglomeration plus
-    time coarsening by nu in one move).
+    Moves: "time", "space" (reference), "time_space" (agglomeration plus
+    time coarsening by nu in one move), and the extensions "space_fw" /
+    "time_space_fw" (full-weighting restriction, (bi)linear interpolation,
+    rediscretised coarse Laplacian: BASELINE config 4's transfers, which the
+    reference does not have).
     """
     cfg = cfg or SolverConfig()
     if n_levels < 2:
@@ -303,6 +334,10 @@ def build_hierarchy(fine: FineSystem, n_levels: int, schedule: str | list[str] =
             levels.append(_space_move(cur))
         elif move == "time_space":
             levels.append(_space_move(cur, time_nu=nu))
+        elif move == "space_fw":
+            levels.append(_space_move_fw(cur))
+        elif move == "time_space_fw":
+            levels.append(_space_move_fw(cur, time_nu=nu))
         else:
             raise ValueError(f"unknown move {move!r}")
         moves.append(move)
@@ -347,6 +382,8 @@ def build_two_level(fine: FineSystem, family: str, nu: int,
 def _child_size(lvl: Level, nxt: Level) -> int:
     """Per-iteration child buffer: the coarse solution, or for MGRIT pairs its
     interpolation to the fine level (ideal interpolation is not a repeat)."""
+    if isinstance(lvl.pair, WeightedSpacePair):  # the solution interpolated in space
+        return lvl.pair.child_size()
     return lvl.total_dim if isinstance(lvl.pair, MgritPair) else nxt.total_dim
 
 
@@ -379,7 +416,7 @@ def _setup_native(hier: LevelHierarchy) -> None:
         lvl = hier.levels[idx]
         nxt = hier.levels[idx + 1]
         ts = None
-        if isinstance(lvl.pair, TimeSpacePair):
+        if isinstance(lvl.pair, (TimeSpacePair, WeightedSpacePair)):
             ts = _empty((lvl.pair.n_T + 1) * lvl.pair.n)
         if idx == 0:
             rhs = hier.fine.rhs.reshape(-1)
@@ -568,7 +605,8 @@ def _fgmres(hier: LevelHierarchy, level_idx: int, rhs, tol: float | None, max_it
         if not st["breakdown"] and last is not None:
             basis.append(last.cpu().numpy() / st["hraw"][n_iter, n_iter - 1])  # IEEE division
         mg = isinstance(lvl.pair, MgritPair)  # cos already hold the interpolated vectors
-        pre = [(vn[l] - (cos[l] if mg else lvl.pair.interpolate(cos[l]))).cpu().numpy()
+        expand = getattr(lvl.pair, "expand_child", lvl.pair.interpolate)
+        pre = [(vn[l] - (cos[l] if mg else expand(cos[l]))).cpu().numpy()
                for l in range(n_iter)]
         report.metadata["basis"] = basis
         report.metadata["preconditioned"] = pre

@@ -218,6 +218,22 @@ MID = {
                         perturb="rowscale", n_cgs=32, max_outer=60),
 }
 
+# EXTENSION cases (no reference counterpart, checked against the oracle's
+# restatement only): full-weighting restriction / (bi)linear interpolation
+# space moves with a rediscretised coarse Laplacian -- the transfers BASELINE
+# config 4 names; the reference agglomerates instead.
+FW = {
+    # config-4 shape, shrunk: theta = 1, two time_space_fw moves, nu = 4 (15 -> 7 -> 3)
+    "fw_c4_small": Case("fw_c4_small", 2, 15, 64, 1.0, 3, ("time_space_fw",) * 2, nu=4,
+                        courant=0.16, u0="modes", max_outer=40),
+    "fw_space_small": Case("fw_space_small", 2, 15, 16, 0.5, 3, ("time", "space_fw"),
+                           courant=0.16, max_outer=40),
+    "fw_1d_small": Case("fw_1d_small", 1, 31, 32, 0.5, 3, ("space_fw", "time"), courant=0.64,
+                        max_outer=40),
+    "fw_dec_small": Case("fw_dec_small", 2, 31, 32, 0.5, 4, ("time", "space_fw", "time"),
+                         courant=0.16, n_cgs=3, max_outer=40),
+}
+
 # BASELINE.json configs (literal) and their regime-adjusted companions.
 BASELINE = {
     "c1": Case("c1", 1, 63, 256, 1.0, 2, ("time",), T=1.0, n_cgs=128),
@@ -230,6 +246,11 @@ BASELINE = {
     "c3_c": Case("c3_c", 2, 63, 512, 0.5, 3, ("time",) * 2, courant=0.16),
     "c4_c": Case("c4_c", 2, 127, 1024, 1.0, 3, ("time_space",) * 2, nu=4, courant=0.16,
                  u0="modes"),
+    # config 4 with the transfers it names (full weighting / bilinear): extension
+    "c4_fw": Case("c4_fw", 2, 127, 1024, 1.0, 3, ("time_space_fw",) * 2, nu=4, T=1.0,
+                  u0="modes"),
+    "c4_fw_c": Case("c4_fw_c", 2, 127, 1024, 1.0, 3, ("time_space_fw",) * 2, nu=4,
+                    courant=0.16, u0="modes"),
     # headline workload: config-5 shape at the paper's Courant number, exact
     # coarsest chain (grid-independent ~19 iterations), FGMRES(30)
     "c5_c": Case("c5_c", 2, 255, 4096, 0.5, 5, ("time",) * 4, courant=0.16, restart=30),

@@ -7,7 +7,7 @@ for q in ${1:-8}; do
   PMK_IPC=$q ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none --print-kernel-base demangled -k "regex:march_tma" -c 420 --csv \
     --log-file gpurun_out/ipc_$q.csv python bench.py --case c5_c --steps 1 --warmup 0 \
-    --e2e-steps 0 --no-cpu-baseline --no-profile > gpurun_out/ipc_$q.log 2>&1
+    --e2e-steps 0 --no-cpu-baseline --no-profile --no-extra > gpurun_out/ipc_$q.log 2>&1
   echo "== PMK_IPC=$q"
   python tools/ncu_summary.py gpurun_out/ipc_$q.csv | grep -E "^\| march" | head -20
 done
