@@ -430,7 +430,7 @@ def matvec_roofline(hier, case, steps: int):
 # at the paper's Courant number, to 1e-8.
 EXTRA = [("c1_c", None), ("c2_c", None), ("c3_c", None), ("c4", 10), ("c4_c", 40),
          ("c5", 30), ("c5_c_dec", None), ("ttts_255", None), ("c1", 12), ("pcr_dec_mid", None),
-         ("line_mid", None), ("line_dec_mid", None)]
+         ("line_mid", None), ("line_dec_mid", None), ("c4_fw", 10), ("c4_fw_c", 40)]
 
 
 def extra_workloads():
