@@ -1006,10 +1006,25 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
     cfg_imv = 0;
     if (const char *e = getenv("PMK_TMA_CFG")) sscanf(e, "%d,%d", &cfg_mvr, &cfg_imv);
   }
+  // Plain matvec tile (tuning knob PMK_MV_CFG; 1: 8x3, 2: 16x2, default by
+  // size).  16-row tiles x 2 stages (92 registers, 2 CTAs/SM) load 18 rows per
+  // 16 outputs instead of 10 per 8: 5.89 vs 5.51 TB/s on the 2.13 GB c5_c
+  // vector (16x3: 5.63, 16x4: 4.88, 24x2: 4.35, 4x3: 5.43, 4x4: 5.31, 8x2:
+  // 5.47; tools/mv_probe.py); launches of a few tens of microseconds prefer
+  // the smaller tile's larger grid (63^2 x 513: 25.0 vs 28.9 us).
+  static const int cfg_mv = [] {
+    const char *e = getenv("PMK_MV_CFG");
+    return e ? atoi(e) : 0;
+  }();
   switch (mode) {
     case kModeMV:
-      if (d2) PMK_RUN(kModeMV, 2, 8, 3, false);
-      else if (wide1d) PMK_RUN(kModeMV, 1, 8, 3, false);
+      if (d2) {
+        const bool tall = cfg_mv ? cfg_mv == 2 : (p.ny >= 64 && N >= ((int64_t)1 << 25));
+        if (tall)
+          PMK_RUN(kModeMV, 2, 16, 2, false);
+        else
+          PMK_RUN(kModeMV, 2, 8, 3, false);
+      } else if (wide1d) PMK_RUN(kModeMV, 1, 8, 3, false);
       else PMK_RUN(kModeMV, 1, 1, 8, false);
       break;
     case kModeMVR:
@@ -1033,7 +1048,9 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
         if (p.fma && !var && scaled && !p.dropped && (cfg_mvr == 0 || cfg_mvr >= 4)) {
           // in-solver K-MVR: 8-row tiles x 3 stages (no pre-pass since the lazy
           // basis, so the taller tile's per-slice savings win over occupancy:
-          // -3% vs 4x3 by ncu, tools/march_ab_env.sh); PMK_TMA_CFG=4/6,x: 8x2, 4x4
+          // -3% vs 4x3 by ncu, tools/march_ab_env.sh; 16x2, the plain matvec's
+          // best tile, is 58% slower here, and 8x2 K-IMV 68% slower than 4x2:
+          // round 2); PMK_TMA_CFG=4/6,x: 8x2, 4x4
           if (cfg_mvr == 4)
             rc = run_tma<kModeMVR, 2, 8, 2, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
@@ -1043,6 +1060,7 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
           else if (cfg_mvr == 7)
             rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
+
           else
             rc = run_tma<kModeMVR, 2, 8, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);

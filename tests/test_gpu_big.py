@@ -111,3 +111,24 @@ def test_dst_gemm_coarsest_beyond_grid_dimension_limits():
     back = fine.matvec(u)
     err = (torch.linalg.vector_norm(back - r) / torch.linalg.vector_norm(r)).item()
     assert err <= 1e-12, err
+
+
+def test_tall_tile_matvec_is_bitwise_the_oracle_matvec():
+    """Vectors of >= 2^25 doubles on grids with >= 64 rows take the 16-row
+    matvec tile (csrc/pmk_march_tma.cu, PMK_MV_CFG): bitwise equal to the
+    oracle's (= the reference's) matvec on 127^2 x 2101 slices, with dropped
+    rows, and on an odd row count that leaves a partial last tile (120)."""
+    from oracle import pintmk_oracle as O
+    import paper_2401_00228_b200 as P
+
+    for nx, ny, steps, dropped in ((127, 127, 2100, (3, 700, 2100)), (150, 120, 1900, ())):
+        op = P.build_laplacian(2, nx, ny)
+        ops = P.build_step_operators(op, P.ThetaSchemeConfig(0.5, 1e-5, steps))
+        sysm = P.BlockBidiagonalSystem(ops.psi, ops.phi, steps, dropped=dropped, grid=(nx, ny),
+                                       dim=2, spectral=ops.spectral_info)
+        assert (steps + 1) * nx * ny >= 1 << 25
+        v = np.random.default_rng(5).standard_normal((steps + 1) * nx * ny)
+        a = O.laplacian(2, nx, ny)[0]
+        d, b = O.blocks_from(a, 0.5, 1e-5)
+        want = O.matvec(O.System(d, b, steps, dropped), v)
+        np.testing.assert_array_equal(sysm.matvec(v), want)
