@@ -1046,13 +1046,17 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
       }
       if (d2) {
         if (p.fma && !var && scaled && !p.dropped && (cfg_mvr == 0 || cfg_mvr >= 4)) {
-          // in-solver K-MVR: 8-row tiles x 3 stages (no pre-pass since the lazy
-          // basis, so the taller tile's per-slice savings win over occupancy:
-          // -3% vs 4x3 by ncu, tools/march_ab_env.sh; 16x2, the plain matvec's
-          // best tile, is 58% slower here, and 8x2 K-IMV 68% slower than 4x2:
-          // round 2); PMK_TMA_CFG=4/6,x: 8x2, 4x4
+          // in-solver K-MVR (no pre-pass since the lazy basis, so taller tiles'
+          // per-slice savings win over occupancy up to a point): 6-row tiles x
+          // 3 stages, 72 registers, 3 CTAs/SM.  Same-box bench A/B, ms of the
+          // K-MVR launches of 4 c5_c solves: 6x3 242, 8x3 249 (round 1's pick,
+          // -3% vs 4x3), 8x4 284, 10x3 / 12x2 ~400 (ptxas goes to > 200
+          // registers), 16x2 397.  PMK_TMA_CFG=4/5/6/7,x: 8x2, 8x3, 4x4, 4x3.
           if (cfg_mvr == 4)
             rc = run_tma<kModeMVR, 2, 8, 2, false, false, true, true>(p, mv, mvt, s, n_partials,
+                                                                       bytes, cat, bulk);
+          else if (cfg_mvr == 5)
+            rc = run_tma<kModeMVR, 2, 8, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
           else if (cfg_mvr == 6)
             rc = run_tma<kModeMVR, 2, 4, 4, false, false, true, true>(p, mv, mvt, s, n_partials,
@@ -1060,9 +1064,8 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
           else if (cfg_mvr == 7)
             rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
-
           else
-            rc = run_tma<kModeMVR, 2, 8, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
+            rc = run_tma<kModeMVR, 2, 6, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
           break;
         }

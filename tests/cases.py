@@ -212,6 +212,10 @@ MID = {
                      perturb="rowscale", max_outer=60),
     "line_dec_mid": Case("line_dec_mid", 2, 127, 32, 1.0, 2, ("time",), courant=0.16,
                          perturb="rowscale", n_cgs=4, max_outer=30),
+    # the headline grid: 255^2 = 65025 unknowns per coarsest slice (two rows
+    # of G_j per warp, 133 MB of Schur-block inverses)
+    "line_255_mid": Case("line_255_mid", 2, 255, 16, 0.5, 2, ("time",), courant=0.16,
+                         perturb="rowscale", max_outer=60),
     # 1-D, 32 decoupled chains (16 slices each) of a non-Toeplitz tridiagonal
     # level: PCR, a CTA per chain
     "pcr_dec_mid": Case("pcr_dec_mid", 1, 1023, 1024, 0.5, 2, ("time",), courant=0.64,

@@ -27,7 +27,8 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
 # cases whose coarsest level takes a kind from csrc/pmk_lines.cu by default
-DEFAULT_KIND = {"line_mid": "line", "line_dec_mid": "line", "pcr_dec_mid": "pcr"}
+DEFAULT_KIND = {"line_mid": "line", "line_dec_mid": "line", "line_255_mid": "line",
+                "pcr_dec_mid": "pcr"}
 
 
 def rel(a, b):
