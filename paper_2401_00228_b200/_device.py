@@ -479,7 +479,6 @@ class CoarseSolver:
         longest = max(b - a for a, b in zip([1] + cuts, cuts + [n_steps + 1])) if n_steps else 0
         one_d = self.ny == 1
         pcr_fits = one_d and self.nx <= PCR_MAX_M and forced not in ("eig", "dense", "dst")
-        fac = None
         if forced == "pcr" and one_d and self.nx <= PCR_MAX_M:
             self._setup_pcr(d, diag, sub, torch)
         elif forced == "line" and not one_d and self.nx <= LINE_MAX_NX:
