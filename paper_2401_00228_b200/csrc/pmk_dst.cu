@@ -43,6 +43,21 @@ namespace {
 #endif
 constexpr int kDstWarps = PMK_DST_WARPS;
 constexpr int kColTile = PMK_DST_COLTILE;
+// Row transforms: smaller CTAs under a register cap keep more warps resident
+// (the kernel is latency-bound at 114 registers x 8 warps x 2 CTAs = 16 warps
+// per SM): 6 warps x 3 CTAs = 18 warps at 96 registers, no spills up to
+// N = 256 (longer transforms keep their registers).  c5_c coarsest solve
+// (tools/coarse_probe.py): 0.472 ms vs 0.499 (8 warps x 2 CTAs), 0.478 (5 x 4),
+// 0.479 (4 x 5).  The
+// column kernel's shared-memory tile keeps it at 2 CTAs either way.
+#ifndef PMK_DST_ROW_WARPS
+#define PMK_DST_ROW_WARPS 6
+#endif
+#ifndef PMK_DST_ROW_BLOCKS
+#define PMK_DST_ROW_BLOCKS 3
+#endif
+constexpr int kRowWarps = PMK_DST_ROW_WARPS;
+constexpr int kRowBlocks = PMK_DST_ROW_BLOCKS;
 
 // e^{-2 pi i j / 32}, j < 32: radix-2 twiddles of every in-register FFT
 // (length L <= 32 uses entries j * 32 / L).
@@ -193,7 +208,7 @@ __device__ __forceinline__ void load_tables(double2 *tw2, double2 *post, const d
 }
 
 template <int LOGN>
-__global__ void __launch_bounds__(32 * kDstWarps)
+__global__ void __launch_bounds__(32 * kRowWarps, LOGN <= 8 ? kRowBlocks : 1)
     dst_rows_kernel(const double *__restrict__ in, double *__restrict__ out, int64_t rows,
                     int64_t rps, int64_t oss, const double2 *gtw2, const double2 *gpost,
                     const int *live) {
@@ -208,8 +223,8 @@ __global__ void __launch_bounds__(32 * kDstWarps)
   double2 *buf = post + N + (warp * P::TPW + h) * P::BS;
   load_tables<LOGN>(tw2, post, gtw2, gpost);
   __syncthreads();
-  const int64_t per_iter = (int64_t)gridDim.x * kDstWarps * P::TPW;
-  for (int64_t r0 = ((int64_t)blockIdx.x * kDstWarps + warp) * P::TPW; r0 < rows;
+  const int64_t per_iter = (int64_t)gridDim.x * kRowWarps * P::TPW;
+  for (int64_t r0 = ((int64_t)blockIdx.x * kRowWarps + warp) * P::TPW; r0 < rows;
        r0 += per_iter) {
     const int64_t r = r0 + h;
     const bool ok = r < rows;
@@ -308,7 +323,8 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
   constexpr int N = P::N;
   const int rc0 = init_constants();
   if (rc0) return rc0;
-  size_t smem = (size_t)(2 * N + kDstWarps * P::TPW * P::BS) * sizeof(double2);
+  constexpr int kWarps = COLS ? kDstWarps : kRowWarps;
+  size_t smem = (size_t)(2 * N + kWarps * P::TPW * P::BS) * sizeof(double2);
   if (COLS) smem += (size_t)(N - 1) * (kColTile + 1) * sizeof(double);
   void (*kern)(const double *, double *, int, int, const double2 *, const double2 *,
                const int *) = dst_cols_kernel<LOGN>;
@@ -322,7 +338,7 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
       PMK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 32 * kDstWarps, smem));
     } else {
       PMK_CUDA_TRY(cudaFuncSetAttribute(kern_r, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      PMK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern_r, 32 * kDstWarps, smem));
+      PMK_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern_r, 32 * kRowWarps, smem));
     }
     occ = b > 0 ? b : 1;
   }
@@ -334,7 +350,7 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
     need = rows_or_slices * ((nx + kColTile - 1) / kColTile);
     elems = (double)rows_or_slices * nx * (N - 1);
   } else {
-    need = (rows_or_slices + kDstWarps * P::TPW - 1) / (kDstWarps * P::TPW);
+    need = (rows_or_slices + kRowWarps * P::TPW - 1) / (kRowWarps * P::TPW);
     elems = (double)rows_or_slices * (N - 1);
   }
   const double units = elems / (N - 1);
@@ -347,7 +363,7 @@ int run_dst(const double *in, double *out, int64_t rows_or_slices, int nx, const
       rps = rows_or_slices;
       oss = rows_or_slices * (N - 1);
     }
-    kern_r<<<grid, 32 * kDstWarps, smem, s>>>(in, out, rows_or_slices, rps, oss, tw2, post,
+    kern_r<<<grid, 32 * kRowWarps, smem, s>>>(in, out, rows_or_slices, rps, oss, tw2, post,
                                               live);
   }
   PMK_LAUNCH_CHECK();
