@@ -97,3 +97,46 @@ def test_pcr_wide_rows_and_many_chains(monkeypatch):
         r = rhs[k] if k in dropped else rhs[k] + b @ ref[k - 1]
         ref[k] = np.linalg.solve(dd, r)
     assert rel(out, ref) <= 1e-12, rel(out, ref)
+
+
+@pytest.mark.parametrize("nx,ny,n_steps,n_cuts", [(100, 37, 6, 0), (300, 9, 5, 2), (40, 50, 40, 30),
+                                                   (255, 12, 4, 0), (17, 130, 7, 3)])
+def test_line_shapes_against_sparse_lu(nx, ny, n_steps, n_cuts, monkeypatch):
+    """Non-square grids, rows per CTA that do not divide nx, lines longer
+    than the register-resident variants (streamed G), and cluster sizes 8 / 4
+    / 2 / 1 (by chain count), against scipy's sparse LU of the same chains
+    (the reference's own coarsest solve, stepper.py:114-146)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as spla
+    import torch
+
+    from paper_2401_00228_b200._device import CoarseSolver, StencilTable
+
+    rng = np.random.default_rng(nx * 1000 + ny)
+    m = nx * ny
+    pat = StencilTable._full_pattern(nx, ny)
+    indptr, indices, slots = pat[0], pat[1], pat[2]
+
+    def five_point(center, off):
+        data = np.where(slots == 2, center + rng.random(slots.size), -off * rng.random(slots.size))
+        return sp.csr_matrix((data, indices.copy(), indptr.copy()), shape=(m, m))
+
+    d = five_point(4.5, 1.0)              # strictly diagonally dominant, non-symmetric
+    b = five_point(0.5, 0.2)
+    dropped = tuple(sorted(int(c) for c in rng.choice(np.arange(2, n_steps + 1), size=n_cuts,
+                                                      replace=False))) if n_cuts else ()
+    monkeypatch.setenv("PMK_COARSE_KIND", "line")
+    cs = CoarseSolver(d, b, n_steps, dropped, 2, nx, ny, None)
+    assert cs.kind == "line"
+    rhs = rng.standard_normal((n_steps + 1, m))
+    out = torch.empty(rhs.size, dtype=torch.float64, device="cuda")
+    cs.solve_into(torch.from_numpy(rhs.ravel()).cuda(), out)
+    out = out.cpu().numpy().reshape(n_steps + 1, m)
+    lu = spla.splu(sp.csc_matrix(d))
+    bt = sp.csr_matrix(b.T)               # 2-D couples with B^T (stepper.py:144)
+    ref = np.empty_like(rhs)
+    ref[0] = rhs[0]
+    for k in range(1, n_steps + 1):
+        r = rhs[k] if k in dropped else rhs[k] + bt @ ref[k - 1]
+        ref[k] = lu.solve(r)
+    assert rel(out, ref) <= 1e-12, rel(out, ref)
