@@ -51,10 +51,21 @@ __global__ void __launch_bounds__(1024)
                      const double *__restrict__ alpha, const double *__restrict__ gamma,
                      const double *__restrict__ inv, int levels, pmk_stencil C,
                      const uint8_t *__restrict__ dropped, const int32_t *__restrict__ seg_start,
-                     int n_seg, const int *live) {
+                     int n_seg, const int *live, int stage_tables) {
   if (!is_live(live)) return;
   extern __shared__ double sh[];
   double *x = sh, *r0 = sh + m, *r1 = sh + 2 * m;
+  // the multipliers of every stride, staged once per CTA when they fit
+  // (2 levels m doubles next to the three rows), else read through L1
+  if (stage_tables) {
+    double *ta = sh + 3 * m, *tg = ta + (size_t)levels * m;
+    for (int i = threadIdx.x; i < levels * m; i += blockDim.x) {
+      ta[i] = alpha[i];
+      tg[i] = gamma[i];
+    }
+    alpha = ta;
+    gamma = tg;
+  }
   const int sg = blockIdx.x;
   const int first = seg_start[sg];
   const int end = (sg + 1 < n_seg) ? seg_start[sg + 1] : n_steps + 1;
@@ -97,8 +108,8 @@ __global__ void __launch_bounds__(1024)
         const int i = tid + e * nt;
         if (i < m) {
           double v = src[i];
-          if (i - s >= 0) v = fma(__ldg(al + i), src[i - s], v);
-          if (i + s < m) v = fma(__ldg(ga + i), src[i + s], v);
+          if (i - s >= 0) v = fma(al[i], src[i - s], v);
+          if (i + s < m) v = fma(ga[i], src[i + s], v);
           dst[i] = v;
         }
       }
@@ -426,8 +437,11 @@ int launch_pcr_chains(const pmk_coarse &C, const double *rhs, double *out, const
   PMK_RETURN_IF(C.dim != 1 || !C.pcr_alpha || !C.pcr_gamma || !C.pcr_inv || !C.seg_start ||
                     C.n_seg < 1 || C.pcr_levels < 0,
                 PMK_ERR_ARG);
-  const size_t smem = 3 * (size_t)m * sizeof(double);
+  size_t smem = 3 * (size_t)m * sizeof(double);
   PMK_RETURN_IF(smem > 220 * 1024, PMK_ERR_UNSUPPORTED);
+  const size_t tabs = 2 * (size_t)C.pcr_levels * m * sizeof(double);
+  const int stage_tables = (C.pcr_levels > 0 && smem + tabs <= 220 * 1024) ? 1 : 0;
+  if (stage_tables) smem += tabs;
   int threads = ((m + 31) / 32) * 32;
   if (threads > 1024) threads = 1024;
   const int E = (m + threads - 1) / threads;
@@ -445,7 +459,7 @@ int launch_pcr_chains(const pmk_coarse &C, const double *rhs, double *out, const
     pcr_chain_kernel<EE><<<C.n_seg, threads, smem, s>>>(rhs, out, m, C.n_steps, C.pcr_alpha,     \
                                                          C.pcr_gamma, C.pcr_inv, C.pcr_levels,   \
                                                          C.coupling, C.dropped, C.seg_start,     \
-                                                         C.n_seg, live);                         \
+                                                         C.n_seg, live, stage_tables);           \
     break;                                                                                       \
   }
   switch (E) {
