@@ -34,6 +34,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <type_traits>
+
 #include "pmk_internal.cuh"
 
 namespace pmk {
@@ -396,6 +398,21 @@ __global__ void __launch_bounds__(kTmaThreads)
         double *ob = (MODE == kModeMVR ? p.v_norm_out : p.out) + kofs + gx0;
         double *hb = (MODE == kModeMVR) ? p.vh + (int64_t)K * m + gx0 : nullptr;
         const bool closes = pos == nu - 1, opens = pos == 0;
+        // The row loop is instantiated per combination of the slice-uniform
+        // flags that steer its stores (a tag of 2 keeps the runtime test):
+        // inside the unrolled loop each test costs a constant-bank reload, a
+        // compare and a branch per row -- half of the ~50 instructions per
+        // output of the in-solver K-MVR (profiles/r2_ncu_march.md).
+        auto rows = [&](auto wn_t, auto inj_t, auto opens_t, auto closes_t, auto wantj_t) {
+          constexpr int kWn = decltype(wn_t)::value, kInj = decltype(inj_t)::value;
+          constexpr int kOp = decltype(opens_t)::value, kCl = decltype(closes_t)::value;
+          constexpr int kWj = decltype(wantj_t)::value;  // K-IMV: 0 none, 1 pj, 3 ||w||^2
+          const bool wn_ = kWn == 2 ? wn : kWn == 1;
+          const bool inj_ = kInj == 2 ? inj : kInj == 1;
+          const bool opens_ = kOp == 2 ? opens : kOp == 1;
+          const bool closes_ = kCl == 2 ? closes : kCl == 1;
+          const bool wantj_ = kWj == 2 ? wantj : kWj == 1;
+          const bool wantw_ = kWj == 2 ? wantw : kWj == 3;
 #pragma unroll
         for (int r = 0; r < RO; ++r) {
           const double *row = col + (r + 1) * kBox + (((r + 1) & 1) ? sh1 : sh0);
@@ -439,18 +456,18 @@ __global__ void __launch_bounds__(kTmaThreads)
             if (MODE == kModeMV) {
               p.out[gi] = o;
             } else if (MODE == kModeMVR) {
-              if (wn) ob[r * nx] = kLazy ? __dmul_rn(cur, osc) : cur;
+              if (wn_) ob[r * nx] = kLazy ? __dmul_rn(cur, osc) : cur;
               if (kSub) wsq = fma(cur, cur, wsq);
               const double sval = FMA ? fma(-p.mu, cur, o) : __dsub_rn(o, __dmul_rn(p.mu, cur));
-              if (inj) {
+              if (inj_) {
                 if (k % nu == 0) {
                   const double sv = kLazy ? __dmul_rn(sval, osc) : sval;
                   p.vh[(int64_t)(k / nu) * m + gx0 + r * nx] = sv;
                   vsq = __dadd_rn(vsq, __dmul_rn(sv, sv));
                 }
               } else {
-                acc[r] = opens ? sval : __dadd_rn(acc[r], sval);
-                if (closes) {
+                acc[r] = opens_ ? sval : __dadd_rn(acc[r], sval);
+                if (closes_) {
                   const double av = kLazy ? __dmul_rn(acc[r], osc) : acc[r];
                   hb[r * nx] = av;
                   vsq = __dadd_rn(vsq, __dmul_rn(av, av));
@@ -461,10 +478,10 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (has_out) ob[r * nx] = o;
               const double v0r = v0_self ? vj[r] : v0v[r];
               if (has_part) dot = FMA ? fma(o, v0r, dot) : __dadd_rn(dot, __dmul_rn(o, v0r));
-              if (wantj) {
+              if (wantj_) {
                 dwj = fma(o, vj[r], dwj);
                 dgj = fma(vj[r], v0r, dgj);
-              } else if (wantw) {
+              } else if (wantw_) {
                 dwj = fma(o, o, dwj);
               }
             }
@@ -472,6 +489,29 @@ __global__ void __launch_bounds__(kTmaThreads)
           qprev[r] = Qu;
           up = cur;
           cur = dn;
+        }
+        };
+        using std::integral_constant;
+        constexpr integral_constant<int, 0> c0{};
+        constexpr integral_constant<int, 1> c1{};
+        constexpr integral_constant<int, 2> rt{};
+        if (MODE == kModeMVR && kSolver && kSub) {  // (sub mode always stores v)
+          if (inj) rows(c1, c1, rt, rt, c0);
+          else if (opens && closes) rows(c1, c0, c1, c1, c0);
+          else if (opens) rows(c1, c0, c1, c0, c0);
+          else if (closes) rows(c1, c0, c0, c1, c0);
+          else rows(c1, c0, c0, c0, c0);
+        } else if (MODE == kModeMVR && kSolver) {
+          if (wn || inj) rows(rt, rt, rt, rt, c0);
+          else if (opens && closes) rows(c0, c0, c1, c1, c0);
+          else if (opens) rows(c0, c0, c1, c0, c0);
+          else if (closes) rows(c0, c0, c0, c1, c0);
+          else rows(c0, c0, c0, c0, c0);
+        } else {
+          // (K-IMV: the same specialisation on its pj / ||w||^2 flags needs 100
+          // registers; capped at the 64 its 4 CTAs per SM allow it spills and
+          // runs 30% slower -- its loop keeps the runtime tests)
+          rows(rt, rt, rt, rt, rt);
         }
       } else if (xin) {
         // ---- generic variant.  Absent neighbours read as 0: adding their
