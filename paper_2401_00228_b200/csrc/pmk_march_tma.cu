@@ -137,7 +137,13 @@ struct TmaGeom {
   int upc, n_chunks;
 };
 
-template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA>
+// IMVK (in-solver K-IMV only) fixes the launch-uniform dot-product flags at
+// compile time, so the row loop carries no test of them: 0 = read them from
+// the parameters; 1 = j = 0 (v is v_0), <w, v_0> only; 2 = j = 0 plus ||w||^2
+// (budget-1 levels); 3 = j >= 1 with the pj dots <w, v_j>, <v_j, v_0>; 4 =
+// j >= 1, <w, v_0> only.
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA,
+          int IMVK = 0>
 __global__ void __launch_bounds__(kTmaThreads)
     march_tma_kernel(const MarchParams p, const __grid_constant__ CUtensorMap tm_v,
                      const __grid_constant__ CUtensorMap tm_vt, const TmaGeom g) {
@@ -175,8 +181,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   double dwj = 0.0, dgj = 0.0;  // K-IMV with pj: <w, v>, <v, v0>
   // (in-solver variant only; run_tma reports it through p.pj_done)
   constexpr bool kPj = MODE == kModeIMV && DIM == 2 && FMA && !VAR && !GATHER;
-  const bool wantj = kPj && p.pj != nullptr && !p.pj_wsq;
-  const bool wantw = kPj && p.pj != nullptr && p.pj_wsq;  // ||w||^2 into slot 0
+  const bool wantj = IMVK ? IMVK == 3 : (kPj && p.pj != nullptr && !p.pj_wsq);
+  const bool wantw = IMVK ? IMVK == 2 : (kPj && p.pj != nullptr && p.pj_wsq);  // ||w||^2 into slot 0
   // In-solver (FMA) launches honour a fixed contract, checked by the
   // launcher: K-IMV writes w (p.out) and the <w, v_0> partials and no x;
   // K-MVR writes the normalised v (p.v_norm_out).  Compile-time flags keep
@@ -198,7 +204,7 @@ __global__ void __launch_bounds__(kTmaThreads)
   const double csub = kSub ? *p.v_sub_coef : 0.0;
   double wsq = 0.0;  // sub mode: ||w - c v_0||^2 of the stored values
   // j = 0 (v is v_0): <w, v_0> takes the staged input itself, no v_0 stream
-  const bool v0_self = kPj && p.v0 == p.v;
+  const bool v0_self = IMVK ? IMVK <= 2 : (kPj && p.v0 == p.v);
   // a lazily scaled v_0 (raw rhs, divisor *v0_scale) is scaled at use
   // a lazily scaled v_0 (raw rhs, divisor *v0_scale): the dot products with
   // it are accumulated raw and scaled once at the end (j >= 1; at j = 0 the
@@ -908,13 +914,14 @@ bool encode_1d(CUtensorMap *map, const double *base, int64_t n) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA = false>
+template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA = false,
+          int IMVK = 0>
 int run_tma(const MarchParams &p, const CUtensorMap &mv, const CUtensorMap &mvt, cudaStream_t s,
             int *n_partials, double bytes, int cat, bool bulk) {
   constexpr int NB = ((MODE == kModeIMV && !GATHER) || (MODE == kModeMVR && GATHER)) ? 2 : 1;
   constexpr int ROWS = (DIM == 2) ? R + 2 : R;
   const size_t smem = (size_t)S * NB * ROWS * kBox * sizeof(double) + 128;
-  auto kern = (DIM == 2) ? march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED, FMA>
+  auto kern = (DIM == 2) ? march_tma_kernel<MODE, DIM, R, S, VAR, GATHER, SCALED, FMA, IMVK>
                          : march_tma_1d_kernel<MODE, R, S, VAR, GATHER, SCALED>;
   static int occ = -1;
   if (occ < 0) {
@@ -1127,11 +1134,29 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
           PMK_RUN(kModeIMV, 2, 4, 3, true);
         } else if (p.fma && !var && cfg_imv == 0 && p.out && !p.x_out && p.partials && p.v0 &&
                    !p.dropped) {
-          rc = scaled ? run_tma<kModeIMV, 2, 4, 2, false, false, true, true>(p, mv, mvt, s,
-                                                                              n_partials, bytes, cat, bulk)
-                      : run_tma<kModeIMV, 2, 4, 2, false, false, false, true>(p, mv, mvt, s,
-                                                                               n_partials, bytes,
-                                                                               cat, bulk);
+          // in-solver K-IMV, one instantiation per dot-product contract (IMVK)
+          const bool self = p.v0 == p.v;
+          int kk = self ? ((p.pj && p.pj_wsq) ? 2 : 1) : ((p.pj && !p.pj_wsq) ? 3 : 4);
+          // (combinations the solver never asks for keep the runtime flags)
+          if ((self && p.pj && !p.pj_wsq) || (!self && p.pj && p.pj_wsq)) kk = 0;
+#define PMK_RUN_IMVK(K)                                                                          \
+  case K:                                                                                        \
+    rc = scaled ? run_tma<kModeIMV, 2, 4, 2, false, false, true, true, K>(p, mv, mvt, s,         \
+                                                                          n_partials, bytes, cat, \
+                                                                          bulk)                  \
+                : run_tma<kModeIMV, 2, 4, 2, false, false, false, true, K>(p, mv, mvt, s,        \
+                                                                           n_partials, bytes,    \
+                                                                           cat, bulk);           \
+    break;
+          switch (kk) {
+            PMK_RUN_IMVK(1)
+            PMK_RUN_IMVK(2)
+            PMK_RUN_IMVK(3)
+            PMK_RUN_IMVK(4)
+            default:
+              PMK_RUN_IMVK(0)
+          }
+#undef PMK_RUN_IMVK
         } else {
           switch (cfg_imv) {
             case 1: PMK_RUN(kModeIMV, 2, 4, 3, false); break;
