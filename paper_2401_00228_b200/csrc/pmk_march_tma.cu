@@ -141,7 +141,9 @@ struct TmaGeom {
 // compile time, so the row loop carries no test of them: 0 = read them from
 // the parameters; 1 = j = 0 (v is v_0), <w, v_0> only; 2 = j = 0 plus ||w||^2
 // (budget-1 levels); 3 = j >= 1 with the pj dots <w, v_j>, <v_j, v_0>; 4 =
-// j >= 1, <w, v_0> only.
+// j >= 1, <w, v_0> only.  For the in-solver K-MVR, IMVK = 1 is the common
+// contract -- v not stored (lazy basis; the sub mode always stores it),
+// time-sum restriction (no MGRIT injection) -- likewise fixed at compile time.
 template <int MODE, int DIM, int R, int S, bool VAR, bool GATHER, bool SCALED, bool FMA,
           int IMVK = 0>
 __global__ void __launch_bounds__(kTmaThreads)
@@ -192,7 +194,8 @@ __global__ void __launch_bounds__(kTmaThreads)
   const bool has_x = kSolver ? false : (p.x_out != nullptr);
   const bool has_part = kSolver ? (MODE == kModeIMV) : (p.partials != nullptr);
   // (K-MVR's normalised v is optional: with a lazy basis nobody stores it)
-  const bool has_vn = p.v_norm_out != nullptr;
+  const bool has_vn = (MODE == kModeMVR && IMVK == 1) ? kSub : p.v_norm_out != nullptr;
+  const bool mvr_inject = (MODE == kModeMVR && IMVK == 1) ? false : p.inject != 0;
   const bool has_drop = !kSolver;  // (solver launches: no dropped rows, no load)
   // In-solver K-MVR works on the raw (unnormalised) staged values: the
   // operator is linear, so A v - mu v = RN(1/h) (A raw - mu raw) up to
@@ -399,7 +402,7 @@ __global__ void __launch_bounds__(kTmaThreads)
         double up = col[sh0];
         double cur = col[kBox + sh1];
         const bool wn = MODE == kModeMVR && has_vn;
-        const bool inj = MODE == kModeMVR && p.inject;
+        const bool inj = MODE == kModeMVR && mvr_inject;
         // slice-k base pointers at (y0, x); rows at + r nx
         double *ob = (MODE == kModeMVR ? p.v_norm_out : p.out) + kofs + gx0;
         double *hb = (MODE == kModeMVR) ? p.vh + (int64_t)K * m + gx0 : nullptr;
@@ -508,7 +511,7 @@ __global__ void __launch_bounds__(kTmaThreads)
           else if (closes) rows(c1, c0, c0, c1, c0);
           else rows(c1, c0, c0, c0, c0);
         } else if (MODE == kModeMVR && kSolver) {
-          if (wn || inj) rows(rt, rt, rt, rt, c0);
+          if (IMVK != 1 && (wn || inj)) rows(rt, rt, rt, rt, c0);
           else if (opens && closes) rows(c0, c0, c1, c1, c0);
           else if (opens) rows(c0, c0, c1, c0, c0);
           else if (closes) rows(c0, c0, c0, c1, c0);
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(kTmaThreads)
               if (has_vn) p.v_norm_out[kofs + gi] = kLazy ? __dmul_rn(cur, osc) : cur;
               if (kSub) wsq = fma(cur, cur, wsq);
               const double sval = __dsub_rn(o, __dmul_rn(p.mu, cur));  // s -= mu v
-              if (p.inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
+              if (mvr_inject) {  // MgritPair.restrict: rows 0, nu, 2 nu, ...
                 if (k % nu == 0) {
                   const double sv = kLazy ? __dmul_rn(sval, osc) : sval;
                   p.vh[(int64_t)(k / nu) * m + gi] = sv;
@@ -1086,6 +1089,9 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
         if (tall)
           rc = run_tma<kModeMVR, 2, 8, 2, false, true, false, true>(p, mv, mvt, s, n_partials,
                                                                      bytes, cat, bulk);
+        else if (!p.inject)
+          rc = run_tma<kModeMVR, 2, 4, 2, false, true, false, true, 1>(p, mv, mvt, s, n_partials,
+                                                                        bytes, cat, bulk);
         else
           rc = run_tma<kModeMVR, 2, 4, 2, false, true, false, true>(p, mv, mvt, s, n_partials,
                                                                      bytes, cat, bulk);
@@ -1111,6 +1117,10 @@ int launch_march_tma(int mode, const MarchParams &p_in, cudaStream_t s, int *n_p
           else if (cfg_mvr == 7)
             rc = run_tma<kModeMVR, 2, 4, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
+          else if (!p.v_norm_out && !p.inject)  // the common contract, fixed at compile time
+            rc = run_tma<kModeMVR, 2, 6, 3, false, false, true, true, 1>(p, mv, mvt, s,
+                                                                          n_partials, bytes, cat,
+                                                                          bulk);
           else
             rc = run_tma<kModeMVR, 2, 6, 3, false, false, true, true>(p, mv, mvt, s, n_partials,
                                                                        bytes, cat, bulk);
