@@ -45,11 +45,13 @@ CPU_SAMPLE = "mid_2d"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--case", default="c5_c")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-warmup", type=int, default=1,
+                    help="untimed end-to-end steps first (allocator / pinned-buffer steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--no-extra", action="store_true",
@@ -294,14 +296,17 @@ def run_ours(args):
     gc.collect()
     torch.cuda.synchronize()
     e2e_t = []
-    for _ in range(max(args.e2e_steps, 0)):
+    n_e2e = max(args.e2e_steps, 0)
+    n_e2e_warm = max(args.e2e_warmup, 0) if n_e2e else 0
+    for i_e2e in range(n_e2e_warm + n_e2e):
         torch.cuda.synchronize()
         pdist.barrier()
         t0 = time.perf_counter()
         h2 = gpu_hierarchy(case, u0=pin_u0)
         xh, rep2 = multilevel_solve(h2, out=pin_x)
         torch.cuda.synchronize()
-        e2e_t.append(time.perf_counter() - t0)
+        if i_e2e >= n_e2e_warm:
+            e2e_t.append(time.perf_counter() - t0)
         del h2, xh
         gc.collect()  # the previous hierarchy's native teardown (cudaFree
         # synchronises) happens here, not inside the next timed step
@@ -374,6 +379,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": 8 * case.m, "d2h_bytes_per_step": 8 * case.N,
                     "seconds_per_step": e2e_s,
                     "step_seconds": [round(t, 4) for t in e2e_t],
+                    "warmup_steps": n_e2e_warm,
                     "includes": "H2D of u0 from pinned memory, hierarchy setup, solve, "
                                 "D2H of x into pinned memory"},
             "roofline": roof,
