@@ -456,15 +456,17 @@ def extra_workloads():
             x, rep = multilevel_solve(h)  # warm-up (graph capture, tables)
             del x
             torch.cuda.synchronize()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for _ in range(reps):
+            times = []
+            for _ in range(reps):  # one event pair per solve; the median is reported
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
                 x, rep = multilevel_solve(h)
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
                 del x
-            e1.record()
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
+            ms = statistics.median(times)
             out[name] = {
                 "unknowns": case.N, "grid": f"{case.nx}x{case.ny}", "n_t": case.n_t,
                 "theta": case.theta, "levels": case.n_levels, "schedule": case.schedule_arg(),
