@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--case", default="c5_c")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-warmup", type=int, default=1,
+    ap.add_argument("--e2e-warmup", type=int, default=2,
                     help="untimed end-to-end steps first (allocator / pinned-buffer steady state)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
