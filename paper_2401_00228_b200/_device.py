@@ -445,6 +445,7 @@ PCR_MAX_CHAIN_VS_DST = 8
 PCR_MAX_CHAIN_VS_EIG = 40
 PCR_MAX_M = 9000      # three shared-memory rows of m doubles per CTA
 LINE_MAX_NX = 1536    # a line is staged by 512 threads x 3 elements
+LINE_MAX_TABLE_BYTES = 16 << 30   # ny nx^2 doubles of inverted Schur blocks (host and device)
 
 
 def forced_coarse_kind() -> str:
@@ -637,6 +638,12 @@ class CoarseSolver:
     def _setup_line(self, d, diag, sub, torch) -> None:
         """Block-Thomas tables of a 2-D 5-point level of any size."""
         dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+        table_bytes = 8 * self.ny * self.nx * self.nx
+        if table_bytes > LINE_MAX_TABLE_BYTES:
+            raise NotImplementedError(
+                f"coarsest level {self.nx}x{self.ny}: the block-Thomas tables of a non-separable "
+                f"operator would take {table_bytes / 2**30:.1f} GiB "
+                f"(limit {LINE_MAX_TABLE_BYTES / 2**30:.0f} GiB); coarsen in space first")
         coef = StencilTable(diag, self.nx, self.ny).coef
         g = line_tables(coef, self.nx, self.ny)
         d.kind = _lib.PMK_COARSE_LINE
