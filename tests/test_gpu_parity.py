@@ -410,3 +410,28 @@ def test_reciprocal_division_is_ieee_bitwise():
         got = out.cpu().numpy()
         same = got.view(np.int64) == ref.view(np.int64)
         assert bool(same.all()), (d, int((~same).sum()))
+
+
+@pytest.mark.parametrize("nx,ny,n_t,levels", [(300, 20, 32, 3), (520, 37, 16, 3), (40, 333, 32, 4)])
+def test_solve_on_split_row_tiles_and_partial_row_tiles(nx, ny, n_t, levels):
+    """Full solves whose in-solver march kernels run with rows split into
+    several column tiles (nx > 255), row counts that leave a partial last
+    6-row / 4-row tile, and non-square grids (dense sine-GEMM coarsest solve),
+    against the oracle: iteration count +-1, x <= 1e-10."""
+    from oracle import pintmk_oracle as O
+    import paper_2401_00228_b200 as P
+
+    rng = np.random.default_rng(nx + ny)
+    h = 1.0 / (nx + 1)
+    dt = 0.16 * h * h / 3.0
+    u0 = rng.standard_normal(nx * ny)
+    op = P.build_laplacian(2, nx, ny)
+    ops = P.build_step_operators(op, P.ThetaSchemeConfig(0.5, dt, n_t))
+    fine = P.FineSystem(ops, u0)
+    cfg = P.SolverConfig(tol=1e-8, max_outer=60)
+    x, rep = P.multilevel_solve(P.build_hierarchy(fine, levels, ["time"] * (levels - 1), cfg, nu=2))
+    oh = O.build(2, nx, ny, 0.5, dt, n_t, u0, levels, ["time"] * (levels - 1),
+                 O.Config(tol=1e-8, max_outer=60), nu=2)
+    xo, info = O.solve(oh)
+    assert abs(rep.outer_iterations - info["iterations"]) <= 1
+    assert rel(x, xo) <= 1e-10, rel(x, xo)
